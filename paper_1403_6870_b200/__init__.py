@@ -1,0 +1,103 @@
+"""paper_1403_6870_b200 -- modified-ziggurat Exponential(1) / N(0,1) sampling on B200.
+
+A B200-native (sm_100a) re-build of the sampling path of the reference package
+`zigfast` (McFarland, arXiv 1403.6870): same Python API (`ExpSampler`,
+`NormalSampler`, `UniformSource`, tables, alias, quality), with every draw
+computed by hand-written CUDA kernels behind a C-ABI (include/zigfast_b200.h).
+
+Convenience surface (SPEC `exponential(size)`, `normal(size)`, `seed(v)`,
+realised in the reference only by its TS frontend) draws from the production
+counter stream of one module-level seed.
+"""
+
+from __future__ import annotations
+
+import threading
+
+from .errors import (BitBudgetExceeded, DeviceError, EmptyWeights, ExtensionMissing,
+                     FormatError, ZigfastError)
+from .quality import EXPECTED_MOMENTS, QualityReport, run_quality
+from .samplers import ExpSampler, NormalSampler, PathCounts
+from .tables import (EXPONENTIAL, HALF_NORMAL, AliasTable, ZigguratTables, build_alias,
+                     default_tables, load, save)
+from .uniform import UniformSource, auto_seed_value, derive_seed, split_index
+
+__version__ = "0.1.0"
+
+_conv_lock = threading.Lock()
+_conv = {"seed": None, "counter": 0}
+
+
+def seed(value: int | None = None) -> int:
+    """(Re)seed the convenience stream; returns the seed in use."""
+    with _conv_lock:
+        _conv["seed"] = (auto_seed_value() if value is None else int(value)) & ((1 << 64) - 1)
+        _conv["counter"] = 0
+        return _conv["seed"]
+
+
+def _convenience(dist_cls, size: int, device=None):
+    with _conv_lock:
+        if _conv["seed"] is None:
+            _conv["seed"] = auto_seed_value()
+        src = UniformSource.counter(_conv["seed"], _conv["counter"])
+        _conv["counter"] += int(size)
+    return dist_cls(source=src, device=device).fill(int(size))
+
+
+def exponential(size: int, device=None):
+    """``size`` Exponential(1) draws (CUDA float64 tensor), continuing the stream."""
+    return _convenience(ExpSampler, size, device)
+
+
+def normal(size: int, device=None):
+    """``size`` N(0,1) draws (CUDA float64 tensor), continuing the stream."""
+    return _convenience(NormalSampler, size, device)
+
+
+def fill_batch(requests, dtype="float64", device=None):
+    """Many independent production requests in ONE launch (BASELINE config 4).
+
+    ``requests``: iterable of (dist, n, seed) or (dist, n, seed, ctr_base) with
+    dist in {"exp", "normal"}.  Returns one CUDA tensor holding the requests
+    back to back (each padded to a 16-byte boundary) and the offsets.
+    """
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    tdtype = torch.float64 if dtype in ("float64", torch.float64) else torch.float32
+    esz = 8 if tdtype == torch.float64 else 4
+    align = 16 // esz
+    reqs = list(requests)
+    arr = (_lib.Request * max(len(reqs), 1))()
+    offsets, off = [], 0
+    for i, r in enumerate(reqs):
+        dist, n, sd = r[0], int(r[1]), int(r[2])
+        base = int(r[3]) if len(r) > 3 else 0
+        arr[i] = _lib.Request(sd & ((1 << 64) - 1), base, n, off,
+                              _lib.EXP if dist in ("exp", "exponential") else _lib.NORMAL, 0)
+        offsets.append(off)
+        off += (n + align - 1) // align * align
+    out = torch.empty(off, dtype=tdtype, device=dev)
+    from .tables import default_tables as _dt
+    tabs = _lib.device_tables(_dt(EXPONENTIAL), _dt(HALF_NORMAL), dev.index)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().zf_fill_batch(tabs.handle, arr, len(reqs),
+                                            _lib.F64 if esz == 8 else _lib.F32, out.data_ptr(),
+                                            _lib.stream_handle(dev)))
+    return out, offsets
+
+
+__all__ = [
+    "AliasTable", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
+    "EmptyWeights", "ExpSampler", "ExtensionMissing", "FormatError", "HALF_NORMAL",
+    "NormalSampler", "PathCounts", "QualityReport", "UniformSource", "ZigfastError",
+    "ZigguratTables", "auto_seed_value", "build_alias", "default_tables", "derive_seed",
+    "exponential", "fill_batch", "load", "normal", "run_quality", "save", "seed",
+    "split_index", "__version__",
+]

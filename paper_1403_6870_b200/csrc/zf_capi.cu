@@ -1,0 +1,224 @@
+// zf_capi.cu -- the extern "C" boundary (include/zigfast_b200.h).
+//
+// Thin: validates arguments, maps them onto the launchers, returns status
+// codes.  Tables are immutable after zf_tables_create, so one handle can be
+// shared by every host thread that targets its device.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+
+#include "zf_internal.h"
+
+namespace zf {
+void xoshiro_pow2_poly(int e, uint64_t out[4]);
+}
+
+using namespace zf;
+
+namespace {
+
+int check_pack(const zf_table_pack* p) {
+  if (!p || !p->sx || !p->xlo || !p->xw || !p->flo || !p->fh || !p->prob || !p->alias)
+    return ZF_EINVAL;
+  if (p->lmax < 1 || p->lmax > 255 || p->nslots != p->lmax + 1) return ZF_ETABLE;
+  for (int64_t k = 0; k < p->nslots; ++k)
+    if (p->alias[k] < 0 || p->alias[k] >= p->nslots) return ZF_ETABLE;
+  return ZF_OK;
+}
+
+void fill_devpack(const zf_table_pack* p, DevPack* d) {
+  std::memset(d, 0, sizeof *d);
+  const int n = (int)p->nslots;
+  for (int i = 0; i < n; ++i) {
+    d->sx[i] = p->sx[i];
+    d->xlo[i] = p->xlo[i];
+    d->xw[i] = p->xw[i];
+    d->flo[i] = p->flo[i];
+    d->fh[i] = p->fh[i];
+    d->prob[i] = p->prob[i];
+    d->alias[i] = (int32_t)p->alias[i];
+  }
+  d->eps = p->eps;
+  d->tailx = p->tailx;
+  d->lmax = (int32_t)p->lmax;
+  d->nslots = (int32_t)p->nslots;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int zf_abi_version(void) { return ZF_ABI_VERSION; }
+
+const char* zf_strerror(int status) {
+  switch (status) {
+    case ZF_OK: return "ok";
+    case ZF_EINVAL: return "invalid argument";
+    case ZF_EDIST: return "unknown distribution, dtype or generator";
+    case ZF_EALIGN: return "unsupported pointer alignment";
+    case ZF_ERANGE: return "counter or size outside the supported range";
+    case ZF_ESHORT: return "replay buffer exhausted (wrap disabled)";
+    case ZF_ETABLE: return "inconsistent table pack";
+    case ZF_EDEVICE: return "no usable sm_100 device";
+    default:
+      return status > 0 ? cudaGetErrorString(static_cast<cudaError_t>(status)) : "unknown status";
+  }
+}
+
+int zf_tables_create(const zf_table_pack* exp_pack, const zf_table_pack* hn_pack, int device,
+                     zf_tables** out) {
+  if (!out) return ZF_EINVAL;
+  *out = nullptr;
+  ZF_TRY_STATUS(check_pack(exp_pack));
+  ZF_TRY_STATUS(check_pack(hn_pack));
+  if (exp_pack->eps < 0.0) return ZF_ETABLE;
+  int ndev = 0;
+  ZF_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return ZF_EDEVICE;
+  cudaDeviceProp prop;
+  ZF_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return ZF_EDEVICE;  // sm_100a cubin only
+  zf_tables* t = new (std::nothrow) zf_tables;
+  if (!t) return ZF_EINVAL;
+  t->device = device;
+  t->sm_count = prop.multiProcessorCount;
+  fill_devpack(exp_pack, &t->host.ex);
+  fill_devpack(hn_pack, &t->host.hn);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&t->dev, sizeof(DevTables));
+  if (e == cudaSuccess) e = cudaMemcpy(t->dev, &t->host, sizeof(DevTables), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (t->dev) cudaFree(t->dev);
+    delete t;
+    return (int)e;
+  }
+  *out = t;
+  return ZF_OK;
+}
+
+int zf_tables_destroy(zf_tables* t) {
+  if (!t) return ZF_OK;
+  cudaError_t e = cudaFree(t->dev);
+  delete t;
+  return cuda_status(e);
+}
+
+int zf_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,
+            void* out_dev, uint64_t n, int64_t* counters_dev, void* stream) {
+  if (!t) return ZF_EINVAL;
+  if (n == 0) return ZF_OK;
+  if (!out_dev) return ZF_EINVAL;
+  if (ctr_base > kMaxCtr || n > kMaxCtr - ctr_base) return ZF_ERANGE;
+  const size_t esz = dtype == ZF_F32 ? 4 : 8;
+  if (reinterpret_cast<uintptr_t>(out_dev) % esz) return ZF_EALIGN;
+  return launch_fill(t, dist, dtype, seed, ctr_base, out_dev, n, counters_dev, as_stream(stream));
+}
+
+int zf_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_base, uint64_t n,
+                  const zf_stats_cfg* cfg, double* partials_dev, unsigned long long* counts_dev,
+                  void* stream) {
+  if (!t || !partials_dev || !counts_dev) return ZF_EINVAL;
+  if (ctr_base > kMaxCtr || n > kMaxCtr - ctr_base) return ZF_ERANGE;
+  return launch_fill_stats(t, dist, seed, ctr_base, n, cfg, partials_dev, counts_dev,
+                           as_stream(stream));
+}
+
+int zf_stats(int dtype, const void* x_dev, uint64_t n, const zf_stats_cfg* cfg,
+             double* partials_dev, unsigned long long* counts_dev, void* stream) {
+  if ((!x_dev && n) || !partials_dev || !counts_dev) return ZF_EINVAL;
+  return launch_stats(dtype, x_dev, n, cfg, partials_dev, counts_dev, as_stream(stream));
+}
+
+uint32_t zf_stats_blocks(uint64_t n) { return stats_blocks(n); }
+
+int zf_fill_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words_dev,
+                   uint64_t nwords, uint64_t cursor, int wrap, void* out_dev, uint64_t n,
+                   zf_path_rec* recs_dev, int64_t* counters_dev, uint64_t* words_consumed,
+                   void* stream) {
+  if (!t || !words_consumed) return ZF_EINVAL;
+  return run_replay(t, dist, dtype, words_dev, nwords, cursor, wrap, out_dev, n, recs_dev,
+                    counters_dev, words_consumed, as_stream(stream));
+}
+
+int zf_words(int gid, uint64_t* state, uint64_t n, uint64_t* words_dev, void* stream) {
+  if (!state || (!words_dev && n)) return ZF_EINVAL;
+  ZF_TRY_STATUS(launch_words(gid, state, n, words_dev, as_stream(stream)));
+  switch (gid) {
+    case ZF_GEN_XOSHIRO256PP: xoshiro_jump_host(state, n); break;
+    case ZF_GEN_SPLITMIX64: state[0] += n * kGamma; break;
+    case ZF_GEN_CTR: state[1] += n; break;
+    default: return ZF_EDIST;
+  }
+  return ZF_OK;
+}
+
+int zf_xoshiro_jump(uint64_t* state, uint64_t k) {
+  if (!state) return ZF_EINVAL;
+  xoshiro_jump_host(state, k);
+  return ZF_OK;
+}
+
+// x^(2^e) mod P(x) of xoshiro256 (test hook for the published jump constants)
+int zf_xoshiro_pow2_poly(int e, uint64_t* out4) {
+  if (!out4 || e < 0 || e > 4096) return ZF_EINVAL;
+  xoshiro_pow2_poly(e, out4);
+  return ZF_OK;
+}
+
+int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* state,
+                const uint64_t* replay_words_dev, uint64_t nwords, void* out_dev, uint64_t n,
+                zf_path_rec* recs_dev, int64_t* counters_dev, void* stream) {
+  if (!t || !state) return ZF_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  if (gid == ZF_GEN_CTR) {
+    if (recs_dev) return ZF_EINVAL;  // production mode has no stream positions
+    ZF_TRY_STATUS(zf_fill(t, dist, dtype, state[0], state[1], out_dev, n, counters_dev, stream));
+    state[1] += n;
+    return ZF_OK;
+  }
+  if (n == 0) return ZF_OK;
+  uint64_t consumed = 0;
+  if (gid == ZF_GEN_REPLAY) {
+    ZF_TRY_STATUS(run_replay(t, dist, dtype, replay_words_dev, nwords, state[0], 1, out_dev, n,
+                             recs_dev, counters_dev, &consumed, s));
+    state[0] += consumed;
+    return ZF_OK;
+  }
+  if (gid != ZF_GEN_XOSHIRO256PP && gid != ZF_GEN_SPLITMIX64) return ZF_EDIST;
+  // sequential generators: materialise a window of the stream on the device,
+  // resolve it like a replay without wrap, then advance the host state by
+  // exactly the words consumed.  Grow the window if it was too short.
+  uint64_t L = n + n / 8 + 4096;
+  for (int attempt = 0; attempt < 8; ++attempt, L *= 2) {
+    uint64_t* words = nullptr;
+    ZF_TRY(cudaMallocAsync(&words, L * sizeof(uint64_t), s));
+    uint64_t st[4] = {state[0], gid == ZF_GEN_XOSHIRO256PP ? state[1] : 0,
+                      gid == ZF_GEN_XOSHIRO256PP ? state[2] : 0,
+                      gid == ZF_GEN_XOSHIRO256PP ? state[3] : 0};
+    int rc = launch_words(gid, st, L, words, s);
+    if (rc == ZF_OK)
+      rc = run_replay(t, dist, dtype, words, L, 0, 0, out_dev, n, recs_dev, counters_dev,
+                      &consumed, s);
+    cudaFreeAsync(words, s);
+    if (rc == ZF_ESHORT) continue;
+    ZF_TRY_STATUS(rc);
+    if (gid == ZF_GEN_XOSHIRO256PP) xoshiro_jump_host(state, consumed);
+    else state[0] += consumed * kGamma;
+    return ZF_OK;
+  }
+  return ZF_ERANGE;
+}
+
+int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
+                  void* out_dev, void* stream) {
+  if (!t || (nreq > 0 && (!reqs || !out_dev))) return ZF_EINVAL;
+  return launch_fill_batch(t, reqs, nreq, dtype, out_dev, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+// zf_fill.cu -- production-mode fill: counter-based words, smem tables,
+// warp-deferred exceptional draws, 128-bit coalesced stores.
+//
+// Replaces the hot loops fill_exp (_kernels.py:226-260) and fill_normal
+// (_kernels.py:597-689).  Work decomposition: a persistent grid of 256-thread
+// CTAs; every warp walks "tiles" of 512 consecutive samples (16 per lane).
+//
+//   pass 1 (fast):  lane l, iteration it, element e handles sample
+//                   base + it*32*V + l*V + e   (V = 16 B / sizeof(out))
+//                   -> one splitmix64 word, byte test, one LDS.64 + I2F + DMUL,
+//                   then a 128-bit store per iteration (the warp writes 512
+//                   contiguous bytes per store instruction).  Samples whose
+//                   byte is >= L_max set a bit in a 16-bit lane mask instead.
+//   pass 2 (rare):  the warp compacts the masked samples (popc + shfl scan)
+//                   into a per-warp smem queue and resolves them 32 at a time,
+//                   one per lane, with the full draw body on the sample's
+//                   secondary counter stream; results are patched in with
+//                   8-byte stores to lines that are still resident in L2.
+//
+// Divergence therefore never stalls pass 1: ~1.2-1.6 % of samples take pass 2
+// and a warp runs pass 2 about once per tile, fully packed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "zf_internal.h"
+#include "zf_tile.cuh"
+
+namespace zf {
+
+template <int DIST, typename OutT, bool COUNTED, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    fill_ctr_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
+                    OutT* __restrict__ out, uint64_t n, unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
+  stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
+              kPacks * (int)sizeof(DevPack));
+  const int lane = threadIdx.x & 31;
+  uint16_t* queue = reinterpret_cast<uint16_t*>(smem_raw + kPacks * sizeof(DevPack)) +
+                    (threadIdx.x >> 5) * kTile;
+  __syncthreads();
+  const DevPack& P = sp[0];
+  const DevPack& E = sp[kPacks - 1];
+
+  LaneCounts lc;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  StoreSink<OutT, VEC> sink{out};
+  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < ntiles;
+       tile += nw)
+    fill_tile<DIST, COUNTED>(P, E, seed, ctr_base, sink, n, tile * kTile, queue, lane, lc);
+  if (COUNTED) flush_counts(lc, counters);
+}
+
+// ---------------------------------------------------------------------------
+// batched requests (config 4): one launch, tiles mapped to requests through a
+// prefix table of per-request tile counts; both packs staged.
+// ---------------------------------------------------------------------------
+
+struct DevRequest {
+  uint64_t seed, ctr_base, n, out_offset;
+  uint64_t tile_begin;  // prefix of tiles
+  int32_t dist, pad;
+};
+
+template <typename OutT, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    fill_batch_kernel(const DevTables* __restrict__ gt, const DevRequest* __restrict__ reqs,
+                      int nreq, uint64_t total_tiles, OutT* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DevTables* st = reinterpret_cast<DevTables*>(smem_raw);
+  stage_block(st, gt, (int)sizeof(DevTables));
+  const int lane = threadIdx.x & 31;
+  uint16_t* queue =
+      reinterpret_cast<uint16_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kTile;
+  __syncthreads();
+  LaneCounts lc;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < total_tiles;
+       tile += nw) {
+    int lo = 0, hi = nreq - 1;  // last request with tile_begin <= tile
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&reqs[mid].tile_begin) <= tile) lo = mid; else hi = mid - 1;
+    }
+    const DevRequest r = reqs[lo];
+    const uint64_t base = (tile - r.tile_begin) * kTile;
+    StoreSink<OutT, VEC> sink{out + r.out_offset};
+    if (r.dist == ZF_EXP)
+      fill_tile<ZF_EXP, false>(st->ex, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue, lane,
+                               lc);
+    else
+      fill_tile<ZF_NORMAL, false>(st->hn, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue,
+                                  lane, lc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch plumbing
+// ---------------------------------------------------------------------------
+
+template <typename K>
+static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid) {
+  static_assert(sizeof(K) > 0, "");
+  int per_sm = 0;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  if (e != cudaSuccess) return (int)e;
+  per_sm = std::max(per_sm, 1);
+  const uint64_t want = (ntiles + kWarps - 1) / kWarps;
+  *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count);
+  if (*grid < 1) *grid = 1;
+  return ZF_OK;
+}
+
+template <int DIST, typename OutT, bool COUNTED, bool VEC>
+static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, OutT* out,
+                        uint64_t n, unsigned long long* counters, cudaStream_t s) {
+  auto kernel = fill_ctr_kernel<DIST, OutT, COUNTED, VEC>;
+  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kTile * sizeof(uint16_t);
+  int grid = 0;
+  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));
+  kernel<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
+  return cuda_status(cudaGetLastError());
+}
+
+template <int DIST, typename OutT>
+static int launch_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base, void* out,
+                       uint64_t n, int64_t* counters, cudaStream_t s) {
+  OutT* o = static_cast<OutT*>(out);
+  const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  auto* c = reinterpret_cast<unsigned long long*>(counters);
+  if (counters)
+    return vec ? launch_typed<DIST, OutT, true, true>(t, seed, ctr_base, o, n, c, s)
+               : launch_typed<DIST, OutT, true, false>(t, seed, ctr_base, o, n, c, s);
+  return vec ? launch_typed<DIST, OutT, false, true>(t, seed, ctr_base, o, n, c, s)
+             : launch_typed<DIST, OutT, false, false>(t, seed, ctr_base, o, n, c, s);
+}
+
+int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,
+                void* out, uint64_t n, int64_t* counters, cudaStream_t s) {
+  if (n == 0) return ZF_OK;
+  if (dist == ZF_EXP && dtype == ZF_F64)
+    return launch_dist<ZF_EXP, double>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_EXP && dtype == ZF_F32)
+    return launch_dist<ZF_EXP, float>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_NORMAL && dtype == ZF_F64)
+    return launch_dist<ZF_NORMAL, double>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_NORMAL && dtype == ZF_F32)
+    return launch_dist<ZF_NORMAL, float>(t, seed, ctr_base, out, n, counters, s);
+  return ZF_EDIST;
+}
+
+template <typename OutT, bool VEC>
+static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq, int nreq,
+                              uint64_t total_tiles, OutT* out, cudaStream_t s) {
+  auto kernel = fill_batch_kernel<OutT, VEC>;
+  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kTile * sizeof(uint16_t);
+  int grid = 0;
+  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_tiles, &grid));
+  kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, nreq, total_tiles, out);
+  return cuda_status(cudaGetLastError());
+}
+
+int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
+                      cudaStream_t s) {
+  if (nreq <= 0) return nreq == 0 ? ZF_OK : ZF_EINVAL;
+  if (dtype != ZF_F64 && dtype != ZF_F32) return ZF_EDIST;
+  const size_t esz = dtype == ZF_F64 ? 8 : 4;
+  // every request must keep 16-byte alignment for the vector path
+  bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  std::vector<DevRequest> h((size_t)nreq);
+  uint64_t tiles = 0;
+  for (int i = 0; i < nreq; ++i) {
+    const zf_request& r = reqs[i];
+    if (r.dist != ZF_EXP && r.dist != ZF_NORMAL) return ZF_EDIST;
+    if (r.ctr_base > kMaxCtr || r.n > kMaxCtr - r.ctr_base) return ZF_ERANGE;
+    if ((r.out_offset * esz) & 15) vec = false;
+    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, tiles, r.dist, 0};
+    tiles += (r.n + kTile - 1) / kTile;
+  }
+  if (tiles == 0) return ZF_OK;
+  DevRequest* d = nullptr;
+  ZF_TRY(cudaMallocAsync(&d, sizeof(DevRequest) * nreq, s));
+  // pageable source: the runtime stages it before returning, so `h` may die
+  cudaError_t e = cudaMemcpyAsync(d, h.data(), sizeof(DevRequest) * nreq,
+                                  cudaMemcpyHostToDevice, s);
+  int status = (int)e;
+  if (e == cudaSuccess) {
+    if (dtype == ZF_F64)
+      status = vec ? launch_batch_typed<double, true>(t, d, nreq, tiles, (double*)out, s)
+                   : launch_batch_typed<double, false>(t, d, nreq, tiles, (double*)out, s);
+    else
+      status = vec ? launch_batch_typed<float, true>(t, d, nreq, tiles, (float*)out, s)
+                   : launch_batch_typed<float, false>(t, d, nreq, tiles, (float*)out, s);
+  }
+  cudaFreeAsync(d, s);
+  return status;
+}
+
+}  // namespace zf

@@ -1,0 +1,55 @@
+// zf_internal.h -- host-side plumbing shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "zf_device.cuh"
+
+struct zf_tables {
+  int device;
+  int sm_count;
+  zf::DevTables* dev;  // device copy: half-normal pack then exponential pack
+  zf::DevTables host;  // host mirror (used by tests of the pack layout)
+};
+
+namespace zf {
+
+// status helpers
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? ZF_OK : (int)e; }
+#define ZF_TRY(expr)                                \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return (int)_e;          \
+  } while (0)
+#define ZF_TRY_STATUS(expr)                         \
+  do {                                              \
+    int _s = (expr);                                \
+    if (_s != ZF_OK) return _s;                     \
+  } while (0)
+
+constexpr uint64_t kMaxCtr = 1ull << 44;  // primary counter range (see zf_device.cuh)
+
+// launchers (zf_fill.cu)
+int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,
+                void* out, uint64_t n, int64_t* counters, cudaStream_t s);
+int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
+                      cudaStream_t s);
+// launchers (zf_stats.cu)
+int launch_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_base, uint64_t n,
+                      const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,
+                      cudaStream_t s);
+int launch_stats(int dtype, const void* x, uint64_t n, const zf_stats_cfg* cfg, double* partials,
+                 unsigned long long* counts, cudaStream_t s);
+uint32_t stats_blocks(uint64_t n);
+// launchers (zf_replay.cu)
+int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, uint64_t nwords,
+               uint64_t cursor, int wrap, void* out, uint64_t n, zf_path_rec* recs,
+               int64_t* counters, uint64_t* consumed, cudaStream_t s);
+int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cudaStream_t s);
+// xoshiro jump-ahead (zf_jump.cpp)
+void xoshiro_jump_host(uint64_t st[4], uint64_t k);
+// polynomials x^(B * 2^i) mod P for i in [0, levels): levels x 4 words
+void xoshiro_jump_polys(uint64_t block_words, int levels, uint64_t* out);
+
+}  // namespace zf

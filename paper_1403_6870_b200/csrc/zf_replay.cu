@@ -1,0 +1,567 @@
+// zf_replay.cu -- oracle mode: the reference's sequential word stream, resolved
+// in parallel; plus device generation of the reference's word streams.
+//
+// The reference consumes ONE word stream with a variable number of words per
+// draw (fill_exp, _kernels.py:226-260; replay source :83-88).  Position p of
+// the stream starts a one-word draw when its low byte is < L_max, unless p lies
+// inside an earlier exceptional draw.  Pipeline over a window of L logical
+// positions (word p = words[(cursor + p) % nwords]):
+//
+//   A  classify + compact   E = sorted positions whose byte >= L_max   (~1.6 %)
+//   B  exceptional draws    full draw body from every e in E, in parallel:
+//                           length, value, path record, counter deltas
+//   C  resolve              e is a real start iff no earlier *real* draw covers
+//                           it.  "Heads" (not covered by any earlier candidate,
+//                           from an exclusive max-scan of e + len) are real;
+//                           between heads a thread walks its short cluster.
+//   D  mark + rank          interior words of real draws are not starts; an
+//                           exclusive scan of start flags gives output ranks
+//   E  emit                 out[rank] = fast value or the exceptional value
+//
+// If the window is too short for n draws, the host doubles L and reruns.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "zf_internal.h"
+
+namespace zf {
+namespace {
+
+constexpr int kRT = 256;              // threads per block
+constexpr int kRI = 8;                // items per thread
+constexpr int kRB = kRT * kRI;        // positions per block
+constexpr uint32_t kIncomplete = 0xFFFFFFFFu;
+
+struct Window {
+  const uint64_t* w;
+  uint64_t nwords, cursor, L;
+  __device__ __forceinline__ uint64_t word(uint64_t p) const {
+    uint64_t idx = cursor + p;
+    if (idx >= nwords) idx %= nwords;
+    return __ldg(reinterpret_cast<const unsigned long long*>(w) + idx);
+  }
+};
+
+// ---- block-wide exclusive scans (256 threads) -------------------------------
+template <typename T, class Op>
+__device__ __forceinline__ T block_exclusive(T v, T identity, Op op, T* smem_warp, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl = op(incl, y);
+  }
+  if (lane == 31) smem_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    T x = lane < nw ? smem_warp[lane] : identity;
+    T xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi = op(xi, y);
+    }
+    if (lane < nw) smem_warp[lane] = xi;  // inclusive per warp
+  }
+  __syncthreads();
+  const T warp_prefix = wid ? smem_warp[wid - 1] : identity;
+  const T excl_in_warp = lane ? __shfl_up_sync(0xffffffffu, incl, 1) : identity;
+  T res = op(warp_prefix, lane ? excl_in_warp : identity);
+  if (total) *total = smem_warp[nw - 1];
+  __syncthreads();
+  return res;
+}
+
+struct Add {
+  template <typename T>
+  __device__ T operator()(T a, T b) const { return a + b; }
+};
+struct Max {
+  template <typename T>
+  __device__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+
+// single-block exclusive scan over `cnt` entries (1024 threads)
+template <typename T, class Op>
+__global__ void scan_single(const T* __restrict__ in, T* __restrict__ out, uint64_t cnt,
+                            T identity, T* __restrict__ total) {
+  __shared__ T warp_buf[32];
+  const uint64_t chunk = (cnt + blockDim.x - 1) / blockDim.x;
+  const uint64_t beg = std::min<uint64_t>(threadIdx.x * chunk, cnt);
+  const uint64_t end = std::min<uint64_t>(beg + chunk, cnt);
+  Op op;
+  T local = identity;
+  for (uint64_t i = beg; i < end; ++i) local = op(local, in[i]);
+  T tot;
+  T run = block_exclusive<T>(local, identity, op, warp_buf, &tot);
+  for (uint64_t i = beg; i < end; ++i) {
+    const T x = in[i];
+    out[i] = run;
+    run = op(run, x);
+  }
+  if (threadIdx.x == 0 && total) *total = tot;
+}
+
+// ---- A: classify / compact ---------------------------------------------------
+__global__ void rp_count_exc(Window win, uint32_t lmax, uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t wb[32];
+  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const uint64_t p = p0 + j;
+    if (p < win.L) c += ((uint32_t)win.word(p) & 0xFFu) >= lmax;
+  }
+  uint32_t tot;
+  block_exclusive<uint32_t>(c, 0u, Add(), wb, &tot);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+}
+
+__global__ void rp_compact_exc(Window win, uint32_t lmax, const uint32_t* __restrict__ boff,
+                               uint32_t* __restrict__ E) {
+  __shared__ uint32_t wb[32];
+  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint32_t flags = 0, c = 0;
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const uint64_t p = p0 + j;
+    const uint32_t f = p < win.L && ((uint32_t)win.word(p) & 0xFFu) >= lmax;
+    flags |= f << j;
+    c += f;
+  }
+  uint32_t o = boff[blockIdx.x] + block_exclusive<uint32_t>(c, 0u, Add(), wb, nullptr);
+#pragma unroll
+  for (int j = 0; j < kRI; ++j)
+    if ((flags >> j) & 1) E[o++] = (uint32_t)(p0 + j);
+}
+
+// ---- B: exceptional draws ------------------------------------------------------
+struct ExcOut {
+  uint32_t* len;
+  double* val;
+  uint32_t* meta;  // layer | path << 8 | attempts << 16
+  uint32_t* cnt;   // [m][6]
+};
+
+template <int DIST>
+__global__ void __launch_bounds__(kRT)
+    rp_draw_exc(const DevTables* __restrict__ gt, Window win, const uint32_t* __restrict__ E,
+                uint32_t m, ExcOut o) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
+  stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
+              kPacks * (int)sizeof(DevPack));
+  __syncthreads();
+  const uint32_t i = blockIdx.x * kRT + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t p = E[i];
+  BufStream s{win.w, win.nwords, win.cursor, p + 1, win.L, 0, false};
+  const uint64_t u = win.word(p);
+  Count c;
+  const double v = draw<DIST>(sp[0], sp[kPacks - 1], u, s, c);
+  o.len[i] = s.over ? kIncomplete : 1u + s.count;
+  o.val[i] = v;
+  o.meta[i] = (uint32_t)(u & 0xFF) | ((uint32_t)c.path << 8) | ((uint32_t)c.attempts << 16);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) o.cnt[(uint64_t)i * 6 + q] = c.c[q];
+}
+
+// ---- C: resolve real starts ------------------------------------------------------
+__device__ __forceinline__ uint64_t reach_of(const uint32_t* E, const uint32_t* len, uint32_t i) {
+  const uint32_t l = len[i];
+  return l == kIncomplete ? ~0ull : (uint64_t)E[i] + l;
+}
+
+__global__ void rp_reach_max(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
+                             uint32_t m, uint64_t* __restrict__ bmax) {
+  __shared__ uint64_t wb[32];
+  const uint64_t i0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint64_t mx = 0;
+  for (int j = 0; j < kRI; ++j)
+    if (i0 + j < m) mx = max(mx, reach_of(E, len, (uint32_t)(i0 + j)));
+  uint64_t tot;
+  block_exclusive<uint64_t>(mx, 0ull, Max(), wb, &tot);
+  if (threadIdx.x == 0) bmax[blockIdx.x] = tot;
+}
+
+__global__ void rp_heads(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
+                         uint32_t m, const uint64_t* __restrict__ bpre, uint8_t* __restrict__ head) {
+  __shared__ uint64_t wb[32];
+  const uint64_t i0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint64_t mx = 0;
+  for (int j = 0; j < kRI; ++j)
+    if (i0 + j < m) mx = max(mx, reach_of(E, len, (uint32_t)(i0 + j)));
+  uint64_t run = max(bpre[blockIdx.x], block_exclusive<uint64_t>(mx, 0ull, Max(), wb, nullptr));
+  for (int j = 0; j < kRI; ++j) {
+    const uint64_t i = i0 + j;
+    if (i >= m) break;
+    head[i] = run <= E[i];
+    run = max(run, reach_of(E, len, (uint32_t)i));
+  }
+}
+
+constexpr int kWalkChunk = 16;
+
+__global__ void rp_walk(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
+                        const uint8_t* __restrict__ head, uint32_t m, uint8_t* __restrict__ real) {
+  const uint64_t beg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kWalkChunk;
+  if (beg >= m) return;
+  const uint64_t end = std::min<uint64_t>(beg + kWalkChunk, m);
+  uint64_t i = beg;
+  while (i < end && !head[i]) ++i;  // leading non-heads belong to the previous walker
+  if (i == end) return;
+  uint64_t cursor = 0;
+  for (; i < m && (i < end || !head[i]); ++i) {
+    const uint8_t r = E[i] >= cursor;
+    real[i] = r;
+    if (r) cursor = reach_of(E, len, (uint32_t)i);
+  }
+}
+
+// ---- D: interior marks -----------------------------------------------------------
+__global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
+                        const uint8_t* __restrict__ real, uint32_t m, uint64_t L,
+                        uint8_t* __restrict__ interior) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || !real[i]) return;
+  const uint64_t p = E[i];
+  const uint64_t stop = len[i] == kIncomplete ? L : std::min<uint64_t>(p + len[i], L);
+  for (uint64_t q = p + 1; q < stop; ++q) interior[q] = 1;
+}
+
+__global__ void rp_count_starts(const uint8_t* __restrict__ interior, uint64_t L,
+                                uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t wb[32];
+  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kRI; ++j)
+    if (p0 + j < L) c += interior[p0 + j] == 0;
+  uint32_t tot;
+  block_exclusive<uint32_t>(c, 0u, Add(), wb, &tot);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+}
+
+// ---- E: emit -------------------------------------------------------------------------
+struct EmitArgs {
+  const uint8_t* interior;
+  const uint32_t* boff_exc;
+  const uint32_t* boff_start;
+  const uint32_t* len;
+  const double* val;
+  const uint32_t* meta;
+  const uint32_t* cnt;
+  uint64_t n;
+  zf_path_rec* recs;
+  unsigned long long* counters;  // internal [6]
+  unsigned long long* consumed;  // internal scalar
+};
+
+template <int DIST, typename OutT>
+__global__ void __launch_bounds__(kRT)
+    rp_emit(const DevTables* __restrict__ gt, Window win, EmitArgs a, OutT* __restrict__ out) {
+  __shared__ uint32_t wb[32];
+  __shared__ double sx[kSlots + 2];
+  __shared__ int lmax_s;
+  const DevPack* P = DIST == ZF_NORMAL ? &gt->hn : &gt->ex;
+  for (int i = threadIdx.x; i < kSlots + 2; i += blockDim.x) sx[i] = P->sx[i];
+  if (threadIdx.x == 0) lmax_s = P->lmax;
+  __syncthreads();
+  const uint32_t lmax = (uint32_t)lmax_s;
+  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+  uint32_t ex_flags = 0, st_flags = 0, ce = 0, cs = 0;
+  uint64_t wds[kRI];
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const uint64_t p = p0 + j;
+    wds[j] = 0;
+    if (p < win.L) {
+      wds[j] = win.word(p);
+      const uint32_t e = ((uint32_t)wds[j] & 0xFFu) >= lmax;
+      const uint32_t s = a.interior[p] == 0;
+      ex_flags |= e << j;
+      st_flags |= s << j;
+      ce += e;
+      cs += s;
+    }
+  }
+  uint32_t eidx = a.boff_exc[blockIdx.x] + block_exclusive<uint32_t>(ce, 0u, Add(), wb, nullptr);
+  uint32_t rank = a.boff_start[blockIdx.x] + block_exclusive<uint32_t>(cs, 0u, Add(), wb, nullptr);
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const bool is_ex = (ex_flags >> j) & 1, is_st = (st_flags >> j) & 1;
+    if (is_st && rank < a.n) {
+      const uint64_t p = p0 + j;
+      double v;
+      uint32_t nw = 1, meta;
+      if (is_ex) {
+        nw = a.len[eidx];
+        v = a.val[eidx];
+        meta = a.meta[eidx];
+        for (int q = 0; q < 6; ++q) c[q] += a.cnt[(uint64_t)eidx * 6 + q];
+      } else {
+        v = fast_value<DIST>(sx, wds[j]);
+        meta = ((uint32_t)wds[j] & 0xFF) | (ZF_PATH_FAST << 8);
+        c[0] += 1;
+        c[1] += 1;
+      }
+      if (nw != kIncomplete) {
+        out[rank] = to_out<OutT>(v);
+        if (a.recs) {
+          zf_path_rec r;
+          r.start = p;
+          r.nwords = nw;
+          r.layer = (uint8_t)(meta & 0xFF);
+          r.path = (uint8_t)((meta >> 8) & 0xFF);
+          r.attempts = (uint16_t)(meta >> 16);
+          a.recs[rank] = r;
+        }
+        if (rank + 1 == a.n) *a.consumed = p + nw;
+      }
+    }
+    eidx += is_ex;
+    rank += is_st;
+  }
+  for (int q = 0; q < 6; ++q) {
+    unsigned long long v = c[q];
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.counters + q, v);
+  }
+}
+
+__global__ void add_counters(const unsigned long long* __restrict__ src,
+                             unsigned long long* __restrict__ dst) {
+  if (threadIdx.x < 6) dst[threadIdx.x] += src[threadIdx.x];
+}
+
+// ---- word generation ---------------------------------------------------------------
+__global__ void words_splitmix(uint64_t state, uint64_t n, uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = mix13(state + (i + 1) * kGamma);
+}
+
+__device__ __forceinline__ void xo_step(uint64_t s[4]) {
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = (s[3] << 45) | (s[3] >> 19);
+}
+
+constexpr int kXoBlock = 1024;  // words per thread
+constexpr int kXoLevels = 40;
+
+// thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0 via the jump
+// polynomials x^(B*2^i) mod P for the set bits of t; output staged through a
+// 32x32 smem tile per warp so stores are coalesced rows.
+__global__ void __launch_bounds__(128)
+    words_xoshiro(ulonglong4 s0, const uint64_t* __restrict__ polys, uint64_t n,
+                  uint64_t* __restrict__ out) {
+  __shared__ uint64_t tile[4][32][33];
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
+  for (int lvl = 0; lvl < kXoLevels; ++lvl) {
+    if (!((t >> lvl) & 1)) continue;
+    uint64_t acc[4] = {0, 0, 0, 0};
+    for (int b = 0; b < 256; ++b) {
+      if ((__ldg(reinterpret_cast<const unsigned long long*>(polys) + lvl * 4 + (b >> 6)) >>
+           (b & 63)) & 1) {
+        acc[0] ^= s[0];
+        acc[1] ^= s[1];
+        acc[2] ^= s[2];
+        acc[3] ^= s[3];
+      }
+      xo_step(s);
+    }
+    s[0] = acc[0];
+    s[1] = acc[1];
+    s[2] = acc[2];
+    s[3] = acc[3];
+  }
+  const uint64_t warp_first = t - lane;  // thread index of lane 0
+  for (int c = 0; c < kXoBlock; c += 32) {
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      tile[wid][lane][j] = ((s[0] + s[3]) << 23 | (s[0] + s[3]) >> 41) + s[0];
+      xo_step(s);
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {  // row r = lane r's 32 consecutive words
+      const uint64_t idx = (warp_first + r) * kXoBlock + c + lane;
+      if (idx < n) out[idx] = tile[wid][r][lane];
+    }
+    __syncwarp();
+  }
+}
+
+struct Workspace {
+  std::vector<void*> ptrs;
+  cudaStream_t s;
+  explicit Workspace(cudaStream_t st) : s(st) {}
+  template <typename T>
+  cudaError_t alloc(T** p, uint64_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMallocAsync(&v, std::max<uint64_t>(count, 1) * sizeof(T), s);
+    if (e == cudaSuccess) ptrs.push_back(v);
+    *p = static_cast<T*>(v);
+    return e;
+  }
+  ~Workspace() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+template <int DIST, typename OutT>
+int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, zf_path_rec* recs,
+                  int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s) {
+  *retry = false;
+  const DevPack& hp = DIST == ZF_NORMAL ? t->host.hn : t->host.ex;
+  const uint32_t lmax = (uint32_t)hp.lmax;
+  const uint64_t L = win.L;
+  const uint32_t nb = (uint32_t)((L + kRB - 1) / kRB);
+  Workspace ws(s);
+  uint32_t *bcnt, *boff, *E, *bcnt2, *boff2;
+  unsigned long long* scal;  // [0] exc total, [1] start total, [2] consumed, [3..8] counters
+  uint8_t* interior;
+  ZF_TRY(ws.alloc(&bcnt, nb));
+  ZF_TRY(ws.alloc(&boff, nb));
+  ZF_TRY(ws.alloc(&bcnt2, nb));
+  ZF_TRY(ws.alloc(&boff2, nb));
+  ZF_TRY(ws.alloc(&scal, 16));
+  ZF_TRY(ws.alloc(&interior, L));
+  ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
+  ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
+  rp_count_exc<<<nb, kRT, 0, s>>>(win, lmax, bcnt);
+  scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt, boff, nb, 0u,
+                                                reinterpret_cast<uint32_t*>(scal));
+  uint32_t m = 0;
+  ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  ZF_TRY(cudaStreamSynchronize(s));
+  ExcOut eo;
+  uint8_t *head, *real;
+  uint64_t *bmax, *bpre;
+  const uint32_t nbE = (m + kRB - 1) / kRB;
+  ZF_TRY(ws.alloc(&E, m));
+  ZF_TRY(ws.alloc(&eo.len, m));
+  ZF_TRY(ws.alloc(&eo.val, m));
+  ZF_TRY(ws.alloc(&eo.meta, m));
+  ZF_TRY(ws.alloc(&eo.cnt, (uint64_t)m * 6));
+  ZF_TRY(ws.alloc(&head, m));
+  ZF_TRY(ws.alloc(&real, m));
+  ZF_TRY(ws.alloc(&bmax, nbE));
+  ZF_TRY(ws.alloc(&bpre, nbE));
+  rp_compact_exc<<<nb, kRT, 0, s>>>(win, lmax, boff, E);
+  if (m) {
+    constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+    const size_t smem = kPacks * sizeof(DevPack);
+    ZF_TRY(cudaFuncSetAttribute(rp_draw_exc<DIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+    rp_draw_exc<DIST><<<(m + kRT - 1) / kRT, kRT, smem, s>>>(t->dev, win, E, m, eo);
+    rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, m, bmax);
+    scan_single<uint64_t, Max><<<1, 1024, 0, s>>>(bmax, bpre, nbE, 0ull, nullptr);
+    rp_heads<<<nbE, kRT, 0, s>>>(E, eo.len, m, bpre, head);
+    ZF_TRY(cudaMemsetAsync(real, 0, m, s));
+    const uint64_t walkers = (m + kWalkChunk - 1) / kWalkChunk;
+    rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, m, real);
+  }
+  ZF_TRY(cudaMemsetAsync(interior, 0, L, s));
+  if (m) rp_mark<<<(m + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, m, L, interior);
+  rp_count_starts<<<nb, kRT, 0, s>>>(interior, L, bcnt2);
+  scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt2, boff2, nb, 0u, nullptr);
+  EmitArgs a{interior, boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
+             scal + 3, scal + 2};
+  rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
+  ZF_TRY(cudaGetLastError());
+  unsigned long long consumed = 0;
+  ZF_TRY(cudaMemcpyAsync(&consumed, scal + 2, sizeof consumed, cudaMemcpyDeviceToHost, s));
+  ZF_TRY(cudaStreamSynchronize(s));
+  if (consumed == ~0ull) {
+    *retry = true;
+    return ZF_OK;
+  }
+  if (counters) add_counters<<<1, 32, 0, s>>>(scal + 3, reinterpret_cast<unsigned long long*>(counters));
+  *consumed_host = consumed;
+  return cuda_status(cudaGetLastError());
+}
+
+template <int DIST, typename OutT>
+int replay_typed(const zf_tables* t, const uint64_t* words, uint64_t nwords, uint64_t cursor,
+                 int wrap, void* out, uint64_t n, zf_path_rec* recs, int64_t* counters,
+                 uint64_t* consumed, cudaStream_t s) {
+  const uint64_t cap = wrap ? (1ull << 32) - kRB : nwords - std::min(cursor, nwords);
+  uint64_t L = std::min<uint64_t>(cap, n + n / 8 + 4096);
+  for (;;) {
+    if (L == 0) return ZF_ESHORT;
+    Window win{words, nwords, wrap ? cursor % nwords : cursor, L};
+    bool retry = false;
+    ZF_TRY_STATUS((replay_window<DIST, OutT>(t, win, out, n, recs, counters, consumed, &retry, s)));
+    if (!retry) return ZF_OK;
+    if (L >= cap) return wrap ? ZF_ERANGE : ZF_ESHORT;
+    L = std::min<uint64_t>(cap, 2 * L);
+  }
+}
+
+}  // namespace
+
+int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, uint64_t nwords,
+               uint64_t cursor, int wrap, void* out, uint64_t n, zf_path_rec* recs,
+               int64_t* counters, uint64_t* consumed, cudaStream_t s) {
+  *consumed = 0;
+  if (n == 0) return ZF_OK;
+  if (!words || nwords == 0 || !out) return ZF_EINVAL;
+  if (n >= (1ull << 31)) return ZF_ERANGE;
+  if (dist == ZF_EXP && dtype == ZF_F64)
+    return replay_typed<ZF_EXP, double>(t, words, nwords, cursor, wrap, out, n, recs, counters,
+                                        consumed, s);
+  if (dist == ZF_EXP && dtype == ZF_F32)
+    return replay_typed<ZF_EXP, float>(t, words, nwords, cursor, wrap, out, n, recs, counters,
+                                       consumed, s);
+  if (dist == ZF_NORMAL && dtype == ZF_F64)
+    return replay_typed<ZF_NORMAL, double>(t, words, nwords, cursor, wrap, out, n, recs,
+                                           counters, consumed, s);
+  if (dist == ZF_NORMAL && dtype == ZF_F32)
+    return replay_typed<ZF_NORMAL, float>(t, words, nwords, cursor, wrap, out, n, recs, counters,
+                                          consumed, s);
+  return ZF_EDIST;
+}
+
+int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cudaStream_t s) {
+  if (n == 0) return ZF_OK;
+  if (gid == ZF_GEN_SPLITMIX64 || gid == ZF_GEN_CTR) {
+    // ctr words are the primary counter stream: splitmix64 of seed from position ctr
+    const uint64_t st = gid == ZF_GEN_CTR ? state[0] + state[1] * kGamma : state[0];
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    words_splitmix<<<grid, 256, 0, s>>>(st, n, out);
+    return cuda_status(cudaGetLastError());
+  }
+  if (gid != ZF_GEN_XOSHIRO256PP) return ZF_EDIST;
+  const uint64_t threads = (n + kXoBlock - 1) / kXoBlock;
+  int levels = 0;
+  while (levels < kXoLevels && (threads - 1) >> levels) ++levels;
+  std::vector<uint64_t> polys((size_t)kXoLevels * 4, 0);
+  xoshiro_jump_polys(kXoBlock, std::max(levels, 1), polys.data());
+  uint64_t* dpolys = nullptr;
+  ZF_TRY(cudaMallocAsync(&dpolys, polys.size() * sizeof(uint64_t), s));
+  cudaError_t e = cudaMemcpyAsync(dpolys, polys.data(), polys.size() * sizeof(uint64_t),
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
+    // round the grid to whole warps so every warp's smem tile is full
+    const uint64_t blocks = (threads + 127) / 128;
+    words_xoshiro<<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(dpolys, s);
+  return cuda_status(e);
+}
+
+}  // namespace zf

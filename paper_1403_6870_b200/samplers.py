@@ -1,0 +1,284 @@
+"""ExpSampler / NormalSampler: the reference's sampling API on B200.
+
+Mirrors `zigfast/exponential.py:23-88` and `zigfast/normal.py:21-88`: same
+constructors, `sample`, `fill`, `fill_counted`, `aggregate`, `path_counts`,
+`reset_counters`, `overhang_attempt`, `tail_start`.  Every draw runs in the
+sm_100a library; the generator id of the source picks the kernel path:
+
+* ``UniformSource(seed, "ctr")`` -- production mode: one asynchronous launch
+  of the counter-stream kernel (`zf_fill`).
+* xoshiro256++ / splitmix64 / replay -- oracle mode: the reference's exact
+  sequential stream, generated and resolved in parallel on the GPU
+  (`zf_fill_gid`), host state advanced exactly as the reference's kernel
+  advances `state` in place.
+
+`fill(out)` accepts an int (returns a new CUDA float64 tensor), a CUDA tensor
+(float64 / float32, filled in place), or a host numpy array / CPU tensor
+(filled through the device, chunked, returned as the same object).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+from .tables import (EXPONENTIAL, HALF_NORMAL, ZigguratTables, build_alias, default_tables)
+from .uniform import CTR_LIMIT, UniformSource
+
+_HOST_CHUNK = 1 << 24  # samples per device chunk when the destination is host memory
+
+
+class PathCounts:
+    """Per-path hit counts (`_packs.py:67-93`); slots as `_kernels.py:23-27`."""
+
+    __slots__ = ("byte_draws", "common", "overhang_fast", "band_evals", "tail", "box_attempts")
+
+    def __init__(self, *vals):
+        for k, v in zip(self.__slots__, vals):
+            setattr(self, k, int(v))
+
+    @classmethod
+    def from_array(cls, arr) -> "PathCounts":
+        return cls(*(int(v) for v in arr))
+
+    def as_tuple(self):
+        return tuple(getattr(self, k) for k in self.__slots__)
+
+    def __eq__(self, other):
+        return isinstance(other, PathCounts) and self.as_tuple() == other.as_tuple()
+
+    def __repr__(self):
+        return "PathCounts(" + ", ".join(f"{k}={getattr(self, k)}" for k in self.__slots__) + ")"
+
+    @property
+    def common_fraction(self) -> float:
+        return self.common / self.byte_draws if self.byte_draws else 0.0
+
+    @property
+    def tail_fraction(self) -> float:
+        return self.tail / self.byte_draws if self.byte_draws else 0.0
+
+    @property
+    def band_eval_fraction(self) -> float:
+        return self.band_evals / self.box_attempts if self.box_attempts else 0.0
+
+
+class _Sampler:
+    _dist: int
+
+    def __init__(self, tables, exp_tables, source, device):
+        import torch
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("samplers run on CUDA devices only (no CPU fallback)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.tables = tables
+        self.exp_tables = exp_tables
+        self.alias = build_alias(tables.a)
+        self.source = source if source is not None else UniformSource()
+        hn = tables if tables.distribution == HALF_NORMAL else default_tables(HALF_NORMAL)
+        self._dev_tables = _lib.device_tables(exp_tables, hn, self.device.index)
+        self._counters = torch.zeros(6, dtype=torch.int64, device=self.device)
+
+    # -- counters ---------------------------------------------------------------
+    @property
+    def counters(self) -> np.ndarray:
+        return self._counters.cpu().numpy()
+
+    @property
+    def path_counts(self) -> PathCounts:
+        return PathCounts.from_array(self.counters)
+
+    def reset_counters(self) -> None:
+        self._counters.zero_()
+
+    # -- core launch --------------------------------------------------------------
+    def _launch(self, dst, counted: bool, recs=None) -> None:
+        """Fill the contiguous CUDA tensor ``dst`` from the source, advancing it."""
+        import torch
+        n = dst.numel()
+        if n == 0:
+            return
+        dtype = {torch.float64: _lib.F64, torch.float32: _lib.F32}.get(dst.dtype)
+        if dtype is None:
+            raise TypeError(f"output dtype must be float64 or float32, got {dst.dtype}")
+        if not dst.is_contiguous():
+            raise ValueError("output tensor must be contiguous")
+        src = self.source
+        if src.gid == _lib.GEN_CTR and int(src.state[1]) + n > CTR_LIMIT:
+            raise ValueError("counter stream exhausted (2^44 samples per seed)")
+        words_ptr, nwords = None, 0
+        if src.gid == _lib.GEN_REPLAY:
+            w = src.replay_words_device(self.device)
+            words_ptr, nwords = w.data_ptr(), w.numel()
+        cnt = self._counters.data_ptr() if counted else None
+        rec_ptr = recs.data_ptr() if recs is not None else None
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().zf_fill_gid(
+                self._dev_tables.handle, self._dist, dtype, src.gid, _lib.u64p(src.state),
+                words_ptr, nwords, dst.data_ptr(), n, rec_ptr, cnt,
+                _lib.stream_handle(self.device)))
+
+    def _fill(self, out, counted: bool):
+        import torch
+        if isinstance(out, (int, np.integer)):
+            if out < 0:
+                raise ValueError("size must be nonnegative")
+            dst = torch.empty(int(out), dtype=torch.float64, device=self.device)
+            self._launch(dst, counted)
+            return dst
+        if isinstance(out, torch.Tensor) and out.is_cuda:
+            if out.device != self.device:
+                raise ValueError(f"output on {out.device}, sampler on {self.device}")
+            self._launch(out.view(-1) if out.is_contiguous() else out, counted)
+            return out
+        # host destination: numpy array or CPU tensor -> through the device in chunks
+        host = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
+        if not isinstance(host, torch.Tensor) or host.is_cuda:
+            raise TypeError("out must be an int, a CUDA tensor, a numpy array or a CPU tensor")
+        if not host.is_contiguous():
+            raise ValueError("host output must be contiguous")
+        self._fill_host(host.view(-1), counted)
+        return out
+
+    def _fill_host(self, host, counted: bool) -> None:
+        """Device fill + D2H copy, double-buffered so chunk i+1 generates while
+        chunk i copies (the copy engine is the bound for host destinations)."""
+        import torch
+        n = host.numel()
+        chunk = min(n, _HOST_CHUNK)
+        if n == 0:
+            return
+        bufs = [torch.empty(chunk, dtype=host.dtype, device=self.device) for _ in range(2)]
+        copy_stream = torch.cuda.Stream(self.device)
+        compute = torch.cuda.current_stream(self.device)
+        done = [None, None]
+        for i, off in enumerate(range(0, n, chunk)):
+            m = min(chunk, n - off)
+            b = i & 1
+            if done[b] is not None:
+                compute.wait_event(done[b])  # buffer b's previous copy finished
+            self._launch(bufs[b][:m], counted)
+            ready = torch.cuda.Event()
+            ready.record(compute)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ready)
+                host[off:off + m].copy_(bufs[b][:m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                done[b] = ev
+        copy_stream.synchronize()
+
+    # -- reference API -------------------------------------------------------------
+    def sample(self) -> float:
+        return float(self._fill(1, False).item())
+
+    def sample_counted(self) -> float:
+        return float(self._fill(1, True).item())
+
+    def fill(self, out):
+        """Fill ``out`` (or a fresh length-``out`` CUDA buffer) with draws."""
+        return self._fill(out, False)
+
+    def fill_counted(self, out):
+        return self._fill(out, True)
+
+    def fill_records(self, n: int):
+        """Oracle mode only: values plus per-sample path records (zf_path_rec)."""
+        import torch
+        if self.source.gid == _lib.GEN_CTR:
+            raise ValueError("path records need a sequential (oracle-mode) source")
+        out = torch.empty(n, dtype=torch.float64, device=self.device)
+        recs = torch.empty(n * _lib.REC_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+        self._launch(out, False, recs=recs)
+        return out, recs.cpu().numpy().view(_lib.REC_DTYPE)
+
+    def aggregate(self, n: int) -> float:
+        """Sum of ``n`` fresh draws (the reference's bench loop).
+
+        Production sources use the fused generate-and-reduce kernel (nothing is
+        written to HBM); sequential sources fill a device buffer and reduce it.
+        The sum is exact-merged across blocks (fsum), so it differs from the
+        reference's left-to-right float sum only by that sum's own rounding.
+        """
+        from .quality import device_sums
+        import torch
+        if n <= 0:
+            return 0.0
+        src = self.source
+        if src.gid == _lib.GEN_CTR:
+            sums, _ = device_sums(self, n, moments=1)
+            return sums[0]
+        total = []
+        left = n
+        while left:
+            m = min(left, _HOST_CHUNK)
+            buf = torch.empty(m, dtype=torch.float64, device=self.device)
+            self._launch(buf, False)
+            from .quality import buffer_sums
+            total.append(buffer_sums(buf, moments=1)[0][0])
+            left -= m
+        return math.fsum(total)
+
+
+class ExpSampler(_Sampler):
+    """Exponential(1) sampler (`exponential.py:23-88`)."""
+
+    _dist = _lib.EXP
+
+    def __init__(self, tables: ZigguratTables | None = None, source: UniformSource | None = None,
+                 device=None):
+        if tables is None:
+            tables = default_tables(EXPONENTIAL)
+        if tables.distribution != EXPONENTIAL:
+            raise ValueError(f"need exponential tables, got {tables.distribution!r}")
+        super().__init__(tables, tables, source, device)
+
+    def overhang_attempt(self, j: int, ux: float, uy: float):
+        """One bounded-box attempt from explicit coordinates (host probe,
+        same arithmetic as the device body); ``(accepted, x, evaluated)``."""
+        if not 1 <= j <= self.tables.l_max:
+            raise IndexError(f"bounded slot out of range: {j}")
+        xl, xr, fb, ft = self.tables.box_bounds(j)
+        xw, fh, eps = xr - xl, ft - fb, float(self.tables.epsilon_max)
+        if ux > 1.0 - uy:
+            ux, uy = 1.0 - uy, 1.0 - ux
+        if uy < 1.0 - ux - eps:
+            return True, xl + ux * xw, False
+        x = xl + ux * xw
+        if fb + uy * fh < np.exp(-x):
+            return True, x, True
+        return False, None, True
+
+
+class NormalSampler(_Sampler):
+    """N(0,1) sampler: half-normal magnitude + sign (`normal.py:21-88`)."""
+
+    _dist = _lib.NORMAL
+
+    def __init__(self, tables: ZigguratTables | None = None, source: UniformSource | None = None,
+                 exp_tables: ZigguratTables | None = None, device=None):
+        if tables is None:
+            tables = default_tables(HALF_NORMAL)
+        if tables.distribution != HALF_NORMAL:
+            raise ValueError(f"need half-normal tables, got {tables.distribution!r}")
+        if exp_tables is None:
+            exp_tables = default_tables(EXPONENTIAL)
+        super().__init__(tables, exp_tables, source, device)
+
+    @property
+    def tail_start(self) -> float:
+        return float(self.tables.x[1])
+
+    def overhang_attempt(self, j: int, ux: float, uy: float):
+        """One plain-rejection box attempt (host probe)."""
+        if not 1 <= j <= self.tables.l_max:
+            raise IndexError(f"bounded slot out of range: {j}")
+        xl, xr, fb, ft = self.tables.box_bounds(j)
+        x = xl + ux * (xr - xl)
+        if fb + uy * (ft - fb) < np.exp(-0.5 * x * x):
+            return True, x, True
+        return False, None, True

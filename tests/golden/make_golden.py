@@ -1,0 +1,178 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run in the build container, where the reference is importable:
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/golden.json.  Nothing at test time reads /root/reference;
+the GPU box only sees this committed file.  Contents (all floats as IEEE-754
+bit patterns in hex, so comparisons are bit-exact):
+
+* the reference's own golden vectors (tests/test_uniform.py:14-23,
+  tests/test_exp_sampler.py:10-16, tests/test_normal_sampler.py:10-16) and its
+  replay known-answer cases (test_exp_sampler.py:93-108,
+  test_normal_sampler.py:54-65), re-derived by calling the reference;
+* alias arrays built by the reference (`alias.py:32-63`) for both tables;
+* config 1 (BASELINE.json): Exponential, n = 1e6, UniformSource(42): SHA-256
+  digests of the values and of the per-sample path records (start offset,
+  words, layer byte, path bits, box attempts), counters, words consumed, plus
+  head/tail samples; the same for the normal sampler on the same stream;
+* production ("ctr") stream samples evaluated BY THE REFERENCE through replay
+  of each sample's word sequence [S(K), S(2^63 + K*2^19 + t) ...];
+* derive_seed values and aggregate() sums.
+"""
+import hashlib
+import json
+import pathlib
+import sys
+
+import numpy as np
+
+from zigfast import ExpSampler, NormalSampler, UniformSource, derive_seed
+from zigfast._packs import make_alias
+from zigfast.tables import default_tables
+
+OUT = pathlib.Path(__file__).resolve().parent / "golden.json"
+M64 = (1 << 64) - 1
+GAMMA = 0x9E3779B97F4A7C15
+
+
+def hexbits(a) -> list:
+    return [format(int(x), "016x") for x in np.asarray(a, dtype=np.float64).view(np.uint64)]
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def mix13(z):
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def splitmix_word(seed, c):
+    return mix13((seed + (c + 1) * GAMMA) & M64)
+
+
+def ctr_words(seed, K, m):
+    base = (1 << 63) + (K << 19)
+    return [splitmix_word(seed, K)] + [splitmix_word(seed, base + t) for t in range(m - 1)]
+
+
+def records(cls, words, n):
+    """Per-sample path records from the reference: replay cursor + counter deltas."""
+    s = cls(source=UniformSource.replay(words))
+    starts = np.empty(n, np.uint64)
+    nw = np.empty(n, np.uint32)
+    layer = np.empty(n, np.uint8)
+    path = np.empty(n, np.uint8)
+    att = np.empty(n, np.uint16)
+    vals = np.empty(n)
+    is_normal = cls is NormalSampler
+    for k in range(n):
+        p0 = int(s.source.state[0])
+        c0 = s.counters.copy()
+        vals[k] = s.sample_counted()
+        d = s.counters - c0
+        starts[k] = p0
+        nw[k] = int(s.source.state[0]) - p0
+        layer[k] = int(words[p0 % len(words)]) & 0xFF
+        bits = 0
+        if d[4]:
+            bits |= 2                       # tail
+        if d[1]:
+            bits |= 1                       # exit through the common path
+        elif d[2]:
+            bits |= 4                       # overhang fast accept (exp)
+        elif not (is_normal and d[4]):
+            bits |= 8                       # accepted after a density evaluation
+        path[k] = bits
+        att[k] = d[5]
+    return vals, starts, nw, layer, path, att, s.counters.copy(), int(s.source.state[0])
+
+
+def main():
+    g = {}
+    g["xoshiro_12345_first8"] = [int(w) for w in UniformSource(12345).next_block(8)]
+    g["xoshiro_42_first64"] = [format(int(w), "016x") for w in UniformSource(42).next_block(64)]
+    g["splitmix_42_first32"] = [format(int(w), "016x")
+                                for w in UniformSource(42, generator="splitmix64").next_block(32)]
+    words = UniformSource(42).next_block(1_100_000)
+    g["xoshiro_42_1p1M_sha256"] = sha(words)
+    src = UniformSource(42)
+    src.next_block(1_000_000)
+    g["xoshiro_42_after_1M_state"] = [format(int(w), "016x") for w in src.state]
+
+    for kind in ("exponential", "halfnormal"):
+        a = make_alias(default_tables(kind))
+        g[f"alias_{kind}_prob"] = hexbits(a.prob)
+        g[f"alias_{kind}_alias"] = [int(x) for x in a.alias]
+
+    for name, cls in (("exp", ExpSampler), ("normal", NormalSampler)):
+        s = cls(source=UniformSource(7))
+        g[f"{name}_seed7_first5"] = hexbits([s.sample() for _ in range(5)])
+        g[f"{name}_seed7_fill3000"] = hexbits(cls(source=UniformSource(7)).fill(3000))
+        g[f"{name}_splitmix99_fill2000"] = hexbits(
+            cls(source=UniformSource(99, generator="splitmix64")).fill(2000))
+        c = cls(source=UniformSource(3))
+        c.fill_counted(200_000)
+        g[f"{name}_seed3_counts200k"] = [int(x) for x in c.counters]
+        g[f"{name}_seed11_aggregate20000"] = format(
+            int(np.float64(cls(source=UniformSource(11)).aggregate(20000)).view(np.uint64)), "016x")
+
+    # replay KATs
+    word = 123456789 << 8
+    e = default_tables("exponential")
+    g["kat_exp_common"] = hexbits([ExpSampler(source=UniformSource.replay([word])).sample()])
+    g["kat_exp_tail"] = hexbits([ExpSampler(source=UniformSource.replay([255, 0, 0, word])).sample()])
+    g["kat_normal_common"] = hexbits([NormalSampler(source=UniformSource.replay([word])).sample()])
+    g["kat_normal_neg"] = hexbits(
+        [NormalSampler(source=UniformSource.replay([(1 << 63) | word])).sample()])
+    g["kat_word"] = word
+    g["exp_x1"] = hexbits([e.x[1]])
+    # wrap-around replay: 7 words, 40 draws (exercises modulo + exceptional)
+    wrapw = [0xFF, 0x12345600, 0x0, 0xFE, 0xABCDEF01, 0x7F00, 0xFFFFFFFFFFFFFFFF]
+    for name, cls in (("exp", ExpSampler), ("normal", NormalSampler)):
+        s = cls(source=UniformSource.replay(wrapw))
+        g[f"{name}_wrap_fill40"] = hexbits(s.fill(40))
+        g[f"{name}_wrap_cursor"] = int(s.source.state[0])
+    g["wrap_words"] = [format(w, "016x") for w in wrapw]
+
+    # config 1 and its normal twin: digests of values and per-sample records
+    n1 = 1_000_000
+    for name, cls in (("exp", ExpSampler), ("normal", NormalSampler)):
+        vals, starts, nw, layer, path, att, cnt, used = records(cls, words, n1)
+        ref = cls(source=UniformSource(42)).fill(n1)
+        assert np.array_equal(ref.view(np.uint64), vals.view(np.uint64))
+        g[f"c1_{name}"] = {
+            "n": n1, "values_sha256": sha(vals), "starts_sha256": sha(starts),
+            "nwords_sha256": sha(nw), "layer_sha256": sha(layer), "path_sha256": sha(path),
+            "attempts_sha256": sha(att) if name == "exp" else None,
+            "counters": [int(x) for x in cnt], "words_consumed": used,
+            "head": hexbits(vals[:64]), "tail": hexbits(vals[-64:]),
+            "n_exceptional": int((nw > 1).sum()),
+        }
+        print(name, "config-1 digests done", cnt, used, file=sys.stderr)
+
+    # production counter stream, evaluated by the reference through replay
+    for name, cls in (("exp", ExpSampler), ("normal", NormalSampler)):
+        out = {}
+        for seed, base, count in ((1234, 0, 4096), (7, 1 << 40, 2048), (99, (1 << 44) - 4096, 4096)):
+            vals = []
+            for k in range(count):
+                w = ctr_words(seed, base + k, 96)
+                s = cls(source=UniformSource.replay(w))
+                vals.append(s.sample())
+                assert int(s.source.state[0]) <= len(w)
+            out[f"{seed}:{base}"] = hexbits(vals)
+        g[f"ctr_{name}"] = out
+
+    g["derive_seed"] = {f"{b}:{s}": derive_seed(b, s) for b in (0, 123, 1234, M64) for s in (0, 1, 7)}
+    OUT.write_text(json.dumps(g, indent=0))
+    print("wrote", OUT, OUT.stat().st_size, "bytes", file=sys.stderr)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+"""Oracle mode on the GPU: the reference's own sequential streams (xoshiro256++,
+splitmix64, replay) resolved in parallel; bit-exact values AND path records."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import assert_bits_equal, bits, hex_to_bits
+
+pytestmark = pytest.mark.gpu
+
+DISTS = ["exp", "normal"]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def zf(cuda):
+    import paper_1403_6870_b200 as zf
+    return zf
+
+
+def cls_of(zf, dist):
+    return zf.ExpSampler if dist == "exp" else zf.NormalSampler
+
+
+def test_xoshiro_words_on_device(zf, golden, cuda):
+    src = zf.UniformSource(12345)
+    assert [int(w) for w in src.next_block(8)] == golden["xoshiro_12345_first8"]
+    src = zf.UniformSource(42)
+    words = src.next_block(1_100_000)
+    assert sha(words) == golden["xoshiro_42_1p1M_sha256"]
+    # block then scalar continues the stream (reference test_uniform.py:136-142)
+    a, b = zf.UniformSource(7), zf.UniformSource(7)
+    a.next_block(13)
+    b.next_block(5)
+    b.next_block(8)
+    assert a.next_u64() == b.next_u64()
+
+
+def test_jump_matches_golden_state(zf, golden):
+    src = zf.UniformSource(42)
+    src.jump(1_000_000)
+    assert [format(int(w), "016x") for w in src.state] == golden["xoshiro_42_after_1M_state"]
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_seed7_golden(zf, golden, cuda, dist):
+    s = cls_of(zf, dist)(source=zf.UniformSource(7), device=cuda)
+    first = [s.sample() for _ in range(5)]
+    assert_bits_equal(first, hex_to_bits(golden[f"{dist}_seed7_first5"]))
+    got = cls_of(zf, dist)(source=zf.UniformSource(7), device=cuda).fill(3000).cpu().numpy()
+    assert_bits_equal(got, hex_to_bits(golden[f"{dist}_seed7_fill3000"]))
+    got = cls_of(zf, dist)(source=zf.UniformSource(99, generator="splitmix64"),
+                           device=cuda).fill(2000).cpu().numpy()
+    assert_bits_equal(got, hex_to_bits(golden[f"{dist}_splitmix99_fill2000"]))
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_fill_equals_repeated_samples(zf, cuda, dist):
+    a = cls_of(zf, dist)(source=zf.UniformSource(7), device=cuda)
+    b = cls_of(zf, dist)(source=zf.UniformSource(7), device=cuda)
+    block = a.fill(300).cpu().numpy()
+    singles = np.array([b.sample() for _ in range(300)])
+    assert np.array_equal(bits(block), bits(singles))
+    # and the host state advanced identically
+    assert np.array_equal(a.source.state, b.source.state)
+
+
+def test_replay_known_answers(zf, golden, cuda):
+    w = golden["kat_word"]
+    U = zf.UniformSource
+    assert_bits_equal([zf.ExpSampler(source=U.replay([w]), device=cuda).sample()],
+                      hex_to_bits(golden["kat_exp_common"]))
+    assert_bits_equal([zf.ExpSampler(source=U.replay([255, 0, 0, w]), device=cuda).sample()],
+                      hex_to_bits(golden["kat_exp_tail"]))
+    assert_bits_equal([zf.NormalSampler(source=U.replay([w]), device=cuda).sample()],
+                      hex_to_bits(golden["kat_normal_common"]))
+    assert_bits_equal([zf.NormalSampler(source=U.replay([(1 << 63) | w]), device=cuda).sample()],
+                      hex_to_bits(golden["kat_normal_neg"]))
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_replay_wraps_like_reference(zf, golden, cuda, dist):
+    s = cls_of(zf, dist)(source=zf.UniformSource.replay(hex_to_bits(golden["wrap_words"])),
+                         device=cuda)
+    got = s.fill(40).cpu().numpy()
+    assert_bits_equal(got, hex_to_bits(golden[f"{dist}_wrap_fill40"]))
+    assert int(s.source.state[0]) == golden[f"{dist}_wrap_cursor"]
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_config1_bit_exact_with_paths(zf, golden, cuda, dist):
+    """BASELINE config 1: n = 1e6 from UniformSource(42).  Values, counters,
+    words consumed and every per-sample path record equal the reference's."""
+    g = golden[f"c1_{dist}"]
+    s = cls_of(zf, dist)(source=zf.UniformSource(42), device=cuda)
+    vals, recs = s.fill_records(g["n"])
+    vals = vals.cpu().numpy()
+    assert_bits_equal(vals[:64], hex_to_bits(g["head"]), "head")
+    assert_bits_equal(vals[-64:], hex_to_bits(g["tail"]), "tail")
+    assert sha(vals) == g["values_sha256"]
+    assert sha(recs["start"]) == g["starts_sha256"]
+    assert sha(recs["nwords"]) == g["nwords_sha256"]
+    assert sha(recs["layer"]) == g["layer_sha256"]
+    assert sha(recs["path"]) == g["path_sha256"]
+    if g["attempts_sha256"]:
+        assert sha(recs["attempts"]) == g["attempts_sha256"]
+    c = cls_of(zf, dist)(source=zf.UniformSource(42), device=cuda)
+    c.fill_counted(g["n"])
+    assert c.counters.tolist() == g["counters"]
+    ref_state = zf.UniformSource(42)
+    ref_state.jump(g["words_consumed"])
+    assert np.array_equal(c.source.state, ref_state.state)
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_records_match_oracle(zf, orc, cuda, dist):
+    n = 200_000
+    s = cls_of(zf, dist)(source=zf.UniformSource(2024, generator="splitmix64"), device=cuda)
+    vals, recs = s.fill_records(n)
+    want, _, wrecs, _ = orc.fill_stream(dist, n, generator="splitmix64", seed=2024, records=True)
+    assert np.array_equal(bits(vals.cpu().numpy()), bits(want))
+    for f in ("start", "nwords", "layer", "path", "attempts"):
+        assert np.array_equal(recs[f], wrecs[f]), f
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_replay_cursor_continues(zf, orc, cuda, dist):
+    words = orc.words("xoshiro256++", 5, 50_000)
+    s = cls_of(zf, dist)(source=zf.UniformSource.replay(words), device=cuda)
+    a = s.fill(10_000).cpu().numpy()
+    b = s.fill(20_000).cpu().numpy()
+    want, _, _, used = orc.fill_stream(dist, 30_000, replay_words=words)
+    assert np.array_equal(bits(np.concatenate([a, b])), bits(want))
+    assert int(s.source.state[0]) == used
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_long_stream_many_windows(zf, orc, cuda, dist):
+    """A fill large enough to need several replay windows (grow + retry)."""
+    n = 3_000_000
+    got = cls_of(zf, dist)(source=zf.UniformSource(77), device=cuda).fill(n).cpu().numpy()
+    want, _, _, _ = orc.fill_stream(dist, n, seed=77)
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_adversarial_replay_all_exceptional(zf, orc, cuda):
+    """Every word exceptional (byte 255): long overlapping draw chains."""
+    rng = np.random.default_rng(0)
+    words = (rng.integers(0, 2**63, 5000, dtype=np.uint64) << np.uint64(8)) | np.uint64(0xFF)
+    words[::7] &= ~np.uint64(0xFF)  # sprinkle a few common-path words
+    for dist in DISTS:
+        s = cls_of(zf, dist)(source=zf.UniformSource.replay(words), device=cuda)
+        got = s.fill(3000).cpu().numpy()
+        want, _, _, used = orc.fill_stream(dist, 3000, replay_words=words)
+        assert np.array_equal(bits(got), bits(want)), dist
+        assert int(s.source.state[0]) == used

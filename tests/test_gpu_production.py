@@ -1,0 +1,146 @@
+"""Production mode on the GPU (counter stream): bit-exact against the CPU oracle
+and against the reference itself (golden ctr fixtures), plus edge cases."""
+import numpy as np
+import pytest
+
+from helpers import assert_bits_equal, bits, hex_to_bits
+
+pytestmark = pytest.mark.gpu
+
+DISTS = ["exp", "normal"]
+
+
+def sampler(zf, dist, seed, counter=0, device=None):
+    cls = zf.ExpSampler if dist == "exp" else zf.NormalSampler
+    return cls(source=zf.UniformSource.counter(seed, counter), device=device)
+
+
+@pytest.fixture(scope="module")
+def zf(cuda):
+    import paper_1403_6870_b200 as zf
+    return zf
+
+
+@pytest.mark.parametrize("dist", DISTS)
+@pytest.mark.parametrize("n", [1, 2, 7, 31, 511, 512, 513, 4096, 100_003])
+def test_fill_matches_oracle(zf, orc, cuda, dist, n):
+    got = sampler(zf, dist, 1234, device=cuda).fill(n).cpu().numpy()
+    want, _, _ = orc.fill_ctr(dist, n, seed=1234)
+    assert_bits_equal(got, bits(want), f"{dist} n={n}")
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_fill_matches_reference_replay(zf, golden, cuda, dist):
+    """Golden values computed by the reference (replay of each sample's words)."""
+    for key, want in golden[f"ctr_{dist}"].items():
+        seed, base = (int(x) for x in key.split(":"))
+        got = sampler(zf, dist, seed, base, device=cuda).fill(len(want)).cpu().numpy()
+        assert_bits_equal(got, hex_to_bits(want), f"ctr {key}")
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_large_counter_offsets(zf, orc, cuda, dist):
+    for base in (1 << 40, 3 << 40, (1 << 44) - 10_000):
+        got = sampler(zf, dist, 7, base, device=cuda).fill(10_000).cpu().numpy()
+        want, _, _ = orc.fill_ctr(dist, 10_000, seed=7, ctr_base=base)
+        assert_bits_equal(got, bits(want), f"base {base}")
+
+
+def test_counter_range_enforced(zf, cuda):
+    s = sampler(zf, "exp", 1, (1 << 44) - 5, device=cuda)
+    with pytest.raises(ValueError):
+        s.fill(10)
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_stream_continuity(zf, cuda, dist):
+    """fill(a); fill(b) == fill(a + b), and equals sample() repeated."""
+    a = sampler(zf, dist, 99, device=cuda)
+    first, second = a.fill(1000).cpu().numpy(), a.fill(2345).cpu().numpy()
+    whole = sampler(zf, dist, 99, device=cuda).fill(3345).cpu().numpy()
+    assert np.array_equal(bits(np.concatenate([first, second])), bits(whole))
+    c = sampler(zf, dist, 99, device=cuda)
+    singles = np.array([c.sample() for _ in range(20)])
+    assert np.array_equal(bits(singles), bits(whole[:20]))
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_float32_is_rounded_float64(zf, cuda, dist):
+    import torch
+    n = 50_001
+    f64 = sampler(zf, dist, 5, device=cuda).fill(n)
+    out = torch.empty(n, dtype=torch.float32, device=cuda)
+    sampler(zf, dist, 5, device=cuda).fill(out)
+    assert torch.equal(out, f64.to(torch.float32))
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_misaligned_and_strided_views(zf, orc, cuda, dist):
+    import torch
+    buf = torch.zeros(10_001, dtype=torch.float64, device=cuda)
+    view = buf[1:]  # 8-byte aligned only: scalar-store kernel variant
+    sampler(zf, dist, 3, device=cuda).fill(view)
+    want, _, _ = orc.fill_ctr(dist, 10_000, seed=3)
+    assert_bits_equal(view.cpu().numpy(), bits(want))
+    assert buf[0].item() == 0.0
+    with pytest.raises(ValueError):
+        sampler(zf, dist, 3, device=cuda).fill(buf[::2])
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_empty_fill(zf, cuda, dist):
+    s = sampler(zf, dist, 3, device=cuda)
+    assert s.fill(0).numel() == 0
+    assert int(s.source.state[1]) == 0
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_host_destinations(zf, orc, cuda, dist):
+    import torch
+    n = (1 << 24) + 77  # more than one host chunk
+    want, _, _ = orc.fill_ctr(dist, n, seed=11)
+    arr = np.zeros(n)
+    out = sampler(zf, dist, 11, device=cuda).fill(arr)
+    assert out is arr
+    assert np.array_equal(bits(arr), bits(want))
+    pinned = torch.empty(1000, dtype=torch.float64).pin_memory()
+    sampler(zf, dist, 11, device=cuda).fill(pinned)
+    assert np.array_equal(bits(pinned.numpy()), bits(want[:1000]))
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_counters_match_oracle(zf, orc, cuda, dist):
+    s = sampler(zf, dist, 21, device=cuda)
+    s.fill_counted(300_000)
+    _, cnt, _ = orc.fill_ctr(dist, 300_000, seed=21)
+    assert s.counters.tolist() == cnt.tolist()
+    c = s.path_counts
+    if dist == "exp":
+        assert c.byte_draws == 300_000 + c.tail
+        assert c.box_attempts == c.overhang_fast + c.band_evals
+    else:
+        assert c.byte_draws == 300_000
+    s.reset_counters()
+    assert s.path_counts.byte_draws == 0
+
+
+def test_batch_matches_individual_fills(zf, orc, cuda):
+    reqs = []
+    for i in range(64):
+        reqs.append(("exp" if i % 2 == 0 else "normal", 8192 if i % 5 else 1000 + i, i))
+    out, offs = zf.fill_batch(reqs, device=cuda)
+    host = out.cpu().numpy()
+    for (dist, n, seed), off in zip(reqs, offs):
+        want, _, _ = orc.fill_ctr(dist, n, seed=seed)
+        assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
+
+
+def test_convenience_api(zf, cuda):
+    zf.seed(2024)
+    a = zf.normal(1000, device=cuda)
+    b = zf.normal(500, device=cuda)
+    zf.seed(2024)
+    c = zf.normal(1500, device=cuda)
+    assert np.array_equal(bits(np.concatenate([a.cpu().numpy(), b.cpu().numpy()])),
+                          bits(c.cpu().numpy()))
+    assert zf.exponential(10, device=cuda).min().item() > 0.0

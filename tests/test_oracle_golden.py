@@ -1,0 +1,136 @@
+"""Pin the CPU oracle to the reference: golden vectors from the reference's own
+tests and fixtures produced by running the reference (tests/golden/make_golden.py)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import assert_bits_equal, bits, hex_to_bits
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# first eight xoshiro256++ outputs for seed 12345 (reference tests/test_uniform.py:14-23)
+GOLDEN_12345 = [10201931350592234856, 3780764549115216544, 1570246627180645737,
+                3237956550421933520, 4899705286669081817, 13385132719381623431,
+                4322154809380817970, 14774873379570401602]
+# reference tests/test_exp_sampler.py:10-16 and tests/test_normal_sampler.py:10-16
+EXP_SEED7 = [0.15069938164952687, 0.70774302052625893, 1.3168329449999849,
+             1.1723584574009387, 1.7174354047860962]
+NORMAL_SEED7 = [0.22612838171099861, 0.88945758308515721, -0.91723712988337558,
+                1.7531374769622967, -0.11601284545578643]
+
+
+def test_xoshiro_golden_words(orc, golden):
+    assert [int(w) for w in orc.words("xoshiro256++", 12345, 8)] == GOLDEN_12345
+    assert golden["xoshiro_12345_first8"] == GOLDEN_12345
+    assert [format(int(w), "016x") for w in orc.words("xoshiro256++", 42, 64)] == \
+        golden["xoshiro_42_first64"]
+    assert sha(orc.words("xoshiro256++", 42, 1_100_000)) == golden["xoshiro_42_1p1M_sha256"]
+
+
+def test_splitmix_words(orc, golden):
+    assert [format(int(w), "016x") for w in orc.words("splitmix64", 42, 32)] == \
+        golden["splitmix_42_first32"]
+
+
+def test_seed7_first_draws(orc):
+    assert list(orc.fill_stream("exp", 5, seed=7)[0]) == EXP_SEED7
+    assert list(orc.fill_stream("normal", 5, seed=7)[0]) == NORMAL_SEED7
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_fill_and_counts_match_reference(orc, golden, dist):
+    assert_bits_equal(orc.fill_stream(dist, 3000, seed=7)[0],
+                      hex_to_bits(golden[f"{dist}_seed7_fill3000"]), "seed 7")
+    assert_bits_equal(orc.fill_stream(dist, 2000, generator="splitmix64", seed=99)[0],
+                      hex_to_bits(golden[f"{dist}_splitmix99_fill2000"]), "splitmix 99")
+    _, cnt, _, _ = orc.fill_stream(dist, 200_000, seed=3)
+    assert cnt.tolist() == golden[f"{dist}_seed3_counts200k"]
+
+
+def test_replay_known_answers(orc, golden):
+    w = golden["kat_word"]
+    assert_bits_equal(orc.fill_stream("exp", 1, replay_words=[w])[0],
+                      hex_to_bits(golden["kat_exp_common"]))
+    assert_bits_equal(orc.fill_stream("exp", 1, replay_words=[255, 0, 0, w])[0],
+                      hex_to_bits(golden["kat_exp_tail"]))
+    assert_bits_equal(orc.fill_stream("normal", 1, replay_words=[w])[0],
+                      hex_to_bits(golden["kat_normal_common"]))
+    assert_bits_equal(orc.fill_stream("normal", 1, replay_words=[(1 << 63) | w])[0],
+                      hex_to_bits(golden["kat_normal_neg"]))
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_replay_wraps(orc, golden, dist):
+    words = hex_to_bits(golden["wrap_words"])
+    vals, _, _, used = orc.fill_stream(dist, 40, replay_words=words)
+    assert_bits_equal(vals, hex_to_bits(golden[f"{dist}_wrap_fill40"]), "wrap")
+    assert used == golden[f"{dist}_wrap_cursor"]
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_config1_values_and_paths(orc, golden, dist):
+    """BASELINE config 1 (n = 1e6, UniformSource(42)): values AND per-sample
+    path records identical to the reference's."""
+    g = golden[f"c1_{dist}"]
+    vals, cnt, recs, used = orc.fill_stream(dist, g["n"], seed=42, records=True)
+    assert sha(vals) == g["values_sha256"]
+    assert cnt.tolist() == g["counters"]
+    assert used == g["words_consumed"]
+    assert sha(recs["start"]) == g["starts_sha256"]
+    assert sha(recs["nwords"]) == g["nwords_sha256"]
+    assert sha(recs["layer"]) == g["layer_sha256"]
+    assert sha(recs["path"]) == g["path_sha256"]
+    if g["attempts_sha256"]:
+        assert sha(recs["attempts"]) == g["attempts_sha256"]
+    assert int((recs["nwords"] > 1).sum()) == g["n_exceptional"]
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_production_stream_matches_reference_replay(orc, golden, dist):
+    """The counter ("ctr") stream restated in C equals the reference run over
+    each sample's word sequence."""
+    for key, want in golden[f"ctr_{dist}"].items():
+        seed, base = (int(x) for x in key.split(":"))
+        vals, _, _ = orc.fill_ctr(dist, len(want), seed=seed, ctr_base=base)
+        assert_bits_equal(vals, hex_to_bits(want), f"ctr {key}")
+
+
+def test_alias_tables_match_reference(orc, golden):
+    hn, ex = orc.packs()
+    for kind, p in (("exponential", ex), ("halfnormal", hn)):
+        assert_bits_equal(p.prob, hex_to_bits(golden[f"alias_{kind}_prob"]), kind)
+        assert p.alias.tolist() == golden[f"alias_{kind}_alias"]
+
+
+def test_derive_seed(orc, golden):
+    for key, want in golden["derive_seed"].items():
+        b, s = (int(x) for x in key.split(":"))
+        assert orc.derive_seed(b, s) == want
+
+
+def test_aggregate_is_sequential_sum(orc, golden):
+    for dist in ("exp", "normal"):
+        got = orc.aggregate(dist, 20000, 11)
+        want = hex_to_bits([golden[f"{dist}_seed11_aggregate20000"]]).view(np.float64)[0]
+        assert got == want
+        vals = orc.fill_stream(dist, 20000, seed=11)[0]
+        acc = 0.0
+        for v in vals:
+            acc += v
+        assert acc == got
+
+
+def test_sharded_baseline_is_reference_sharding(orc):
+    """The CPU baseline's threads reproduce quality.py's derive_seed sharding."""
+    n, threads = 10_000, 4
+    out = orc.fill_sharded("exp", n, 5, threads=threads)
+    off = 0
+    for i in range(threads):
+        share = n // threads + (1 if i < n % threads else 0)
+        want = orc.fill_stream("exp", share, seed=orc.derive_seed(5, i))[0]
+        assert np.array_equal(bits(out[off:off + share]), bits(want))
+        off += share
