@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "zf_internal.h"
@@ -68,8 +70,8 @@ __device__ __forceinline__ T block_exclusive(T v, T identity, Op op, T* smem_war
   }
   __syncthreads();
   const T warp_prefix = wid ? smem_warp[wid - 1] : identity;
-  const T excl_in_warp = lane ? __shfl_up_sync(0xffffffffu, incl, 1) : identity;
-  T res = op(warp_prefix, lane ? excl_in_warp : identity);
+  const T up = __shfl_up_sync(0xffffffffu, incl, 1);  // all 32 lanes must execute it
+  T res = op(warp_prefix, lane ? up : identity);
   if (total) *total = smem_warp[nw - 1];
   __syncthreads();
   return res;
@@ -403,6 +405,17 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ZF_DEBUG=1: synchronise and report after every pipeline stage (stderr)
+static bool debug_on() {
+  static const bool on = getenv("ZF_DEBUG") != nullptr;
+  return on;
+}
+static void dbg(const char* what, cudaStream_t s) {
+  if (!debug_on()) return;
+  cudaError_t e = cudaStreamSynchronize(s);
+  fprintf(stderr, "[zf] %-16s %s\n", what, cudaGetErrorString(e));
+}
+
 struct Workspace {
   std::vector<void*> ptrs;
   cudaStream_t s;
@@ -424,6 +437,9 @@ template <int DIST, typename OutT>
 int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, zf_path_rec* recs,
                   int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s) {
   *retry = false;
+  if (debug_on()) fprintf(stderr, "[zf] replay_window L=%llu nwords=%llu cursor=%llu n=%llu\n",
+                          (unsigned long long)win.L, (unsigned long long)win.nwords,
+                          (unsigned long long)win.cursor, (unsigned long long)n);
   const DevPack& hp = DIST == ZF_NORMAL ? t->host.hn : t->host.ex;
   const uint32_t lmax = (uint32_t)hp.lmax;
   const uint64_t L = win.L;
@@ -438,11 +454,14 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(ws.alloc(&boff2, nb));
   ZF_TRY(ws.alloc(&scal, 16));
   ZF_TRY(ws.alloc(&interior, L));
+  if (debug_on()) fprintf(stderr, "[zf] workspace allocated\n");
   ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
   ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
   rp_count_exc<<<nb, kRT, 0, s>>>(win, lmax, bcnt);
+  dbg("rp_count_exc", s);
   scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt, boff, nb, 0u,
                                                 reinterpret_cast<uint32_t*>(scal));
+  dbg("scan_exc", s);
   uint32_t m = 0;
   ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   ZF_TRY(cudaStreamSynchronize(s));
@@ -460,26 +479,34 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(ws.alloc(&bmax, nbE));
   ZF_TRY(ws.alloc(&bpre, nbE));
   rp_compact_exc<<<nb, kRT, 0, s>>>(win, lmax, boff, E);
+  dbg("rp_compact_exc", s);
   if (m) {
     constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
     const size_t smem = kPacks * sizeof(DevPack);
     ZF_TRY(cudaFuncSetAttribute(rp_draw_exc<DIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
     rp_draw_exc<DIST><<<(m + kRT - 1) / kRT, kRT, smem, s>>>(t->dev, win, E, m, eo);
+  dbg("rp_draw_exc<DIST>", s);
     rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, m, bmax);
+  dbg("rp_reach_max", s);
     scan_single<uint64_t, Max><<<1, 1024, 0, s>>>(bmax, bpre, nbE, 0ull, nullptr);
     rp_heads<<<nbE, kRT, 0, s>>>(E, eo.len, m, bpre, head);
+  dbg("rp_heads", s);
     ZF_TRY(cudaMemsetAsync(real, 0, m, s));
     const uint64_t walkers = (m + kWalkChunk - 1) / kWalkChunk;
     rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, m, real);
+  dbg("rp_walk", s);
   }
   ZF_TRY(cudaMemsetAsync(interior, 0, L, s));
   if (m) rp_mark<<<(m + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, m, L, interior);
+  dbg("rp_mark", s);
   rp_count_starts<<<nb, kRT, 0, s>>>(interior, L, bcnt2);
+  dbg("rp_count_starts", s);
   scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt2, boff2, nb, 0u, nullptr);
   EmitArgs a{interior, boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
              scal + 3, scal + 2};
   rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
+  dbg("OutT>", s);
   ZF_TRY(cudaGetLastError());
   unsigned long long consumed = 0;
   ZF_TRY(cudaMemcpyAsync(&consumed, scal + 2, sizeof consumed, cudaMemcpyDeviceToHost, s));
