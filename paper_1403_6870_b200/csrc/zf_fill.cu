@@ -39,19 +39,17 @@ __global__ void __launch_bounds__(kThreads)
   stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
               kPacks * (int)sizeof(DevPack));
   const int lane = threadIdx.x & 31;
-  uint16_t* queue = reinterpret_cast<uint16_t*>(smem_raw + kPacks * sizeof(DevPack)) +
-                    (threadIdx.x >> 5) * kTile;
+  uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kPacks * sizeof(DevPack)) +
+                    (threadIdx.x >> 5) * kQueueCap;
   __syncthreads();
   const DevPack& P = sp[0];
   const DevPack& E = sp[kPacks - 1];
 
   LaneCounts lc;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   StoreSink<OutT, VEC> sink{out};
-  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < ntiles;
-       tile += nw)
-    fill_tile<DIST, COUNTED>(P, E, seed, ctr_base, sink, n, tile * kTile, queue, lane, lc);
+  run_tiles<DIST, COUNTED>(P, E, seed, ctr_base, sink, n,
+                           (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
+                           (uint64_t)gridDim.x * kWarps, queue, lane, lc);
   if (COUNTED) flush_counts(lc, counters);
 }
 
@@ -74,8 +72,8 @@ __global__ void __launch_bounds__(kThreads)
   DevTables* st = reinterpret_cast<DevTables*>(smem_raw);
   stage_block(st, gt, (int)sizeof(DevTables));
   const int lane = threadIdx.x & 31;
-  uint16_t* queue =
-      reinterpret_cast<uint16_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kTile;
+  uint32_t* queue =
+      reinterpret_cast<uint32_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kTile;
   __syncthreads();
   LaneCounts lc;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
@@ -123,7 +121,7 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
                         uint64_t n, unsigned long long* counters, cudaStream_t s) {
   auto kernel = fill_ctr_kernel<DIST, OutT, COUNTED, VEC>;
   constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
-  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kTile * sizeof(uint16_t);
+  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
@@ -161,7 +159,7 @@ template <typename OutT, bool VEC>
 static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq, int nreq,
                               uint64_t total_tiles, OutT* out, cudaStream_t s) {
   auto kernel = fill_batch_kernel<OutT, VEC>;
-  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kTile * sizeof(uint16_t);
+  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kTile * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_tiles, &grid));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, nreq, total_tiles, out);

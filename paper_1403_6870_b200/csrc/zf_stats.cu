@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
   StatsShared* sh = reinterpret_cast<StatsShared*>(smem_raw + kPacks * sizeof(DevPack));
-  uint16_t* queue = reinterpret_cast<uint16_t*>(sh + 1) + (threadIdx.x >> 5) * kTile;
+  uint32_t* queue = reinterpret_cast<uint32_t*>(sh + 1) + (threadIdx.x >> 5) * kQueueCap;
   stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
               kPacks * (int)sizeof(DevPack));
   StatsSink sink;
@@ -80,12 +80,9 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   LaneCounts lc;
   const int lane = threadIdx.x & 31;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < ntiles;
-       tile += nw)
-    fill_tile<DIST, false>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, tile * kTile, queue,
-                           lane, lc);
+  run_tiles<DIST, false>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n,
+                         (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
+                         (uint64_t)gridDim.x * kWarps, queue, lane, lc);
   __syncthreads();
   flush_sink(sink, sh, cfg, partials, counts);
 }
@@ -125,7 +122,7 @@ int launch_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_
                       cudaStream_t s) {
   ZF_TRY_STATUS(check_cfg(cfg));
   const uint32_t grid = stats_blocks(n);
-  const size_t queue = (size_t)kWarps * kTile * sizeof(uint16_t);
+  const size_t queue = (size_t)kWarps * kQueueCap * sizeof(uint32_t);
   if (dist == ZF_EXP) {
     const size_t smem = sizeof(DevPack) + sizeof(StatsShared) + queue;
     ZF_TRY(cudaFuncSetAttribute(fill_stats_kernel<ZF_EXP>,

@@ -92,13 +92,14 @@ struct StatsSink {
   }
 };
 
-// One warp tile: samples [base, min(base + kTile, n)) of the counter stream
-// (seed, ctr_base); pass 1 = fast path for all, pass 2 = compacted exceptions.
+// Pass 1 of one warp tile: samples [base, min(base + kTile, n)) of the
+// counter stream (seed, ctr_base).  Every lane computes the fast-path value of
+// its 16 samples and hands V of them at a time to the sink; returns the lane's
+// mask of exceptional samples (bit it*V + e  <->  offset it*32*V + lane*V + e).
 template <int DIST, bool COUNTED, class Sink>
-__device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, uint64_t seed,
-                                          uint64_t ctr_base, Sink& sink, uint64_t n,
-                                          uint64_t base, uint16_t* queue, int lane,
-                                          LaneCounts& lc) {
+__device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, uint64_t ctr_base,
+                                              Sink& sink, uint64_t n, uint64_t base, int lane,
+                                              LaneCounts& lc) {
   using OutT = typename Sink::Out;
   constexpr int V = Sink::V;
   constexpr int kIters = kPerLane / V;
@@ -108,7 +109,6 @@ __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, ui
   const uint64_t k_lane = base + (uint64_t)lane * V;
   const uint64_t st0 = seed + (ctr_base + k_lane + 1) * kGamma;
   uint32_t mask = 0;
-
   if (base + kTile <= n) {
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
@@ -152,43 +152,108 @@ __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, ui
       lc.c[1] += fast;
     }
   }
+  return mask;
+}
 
-  // ---- pass 2: compact the exceptional samples of the whole warp ----------
-  const int mine = __popc(mask);
+// Pass 2 body for one exceptional sample k: the full draw on its secondary
+// counter stream, written through the sink.
+template <int DIST, bool COUNTED, class Sink>
+__device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, uint64_t seed,
+                                            uint64_t ctr_base, Sink& sink, uint64_t k,
+                                            LaneCounts& lc) {
+  using OutT = typename Sink::Out;
+  const uint64_t K = ctr_base + k;
+  const uint64_t u = mix13(seed + (K + 1) * kGamma);
+  CtrStream s{seed + (kExcBase + (K << kExcShift)) * kGamma};
+  double v;
+  if (COUNTED) {
+    Count c;
+    v = draw<DIST>(P, E, u, s, c);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) lc.c[q] += c.c[q];
+  } else {
+    NoCount c;
+    v = draw<DIST>(P, E, u, s, c);
+  }
+  sink.put(k, to_out<OutT>(v), false);
+}
+
+// Exclusive warp prefix of `mine`; returns it and sets *total (warp-uniform).
+__device__ __forceinline__ int warp_excl_scan(int mine, int lane, int* total) {
   int incl = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += y;
   }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  *total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - mine;
+}
+
+template <int V>
+__device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
+  return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
+}
+
+// One warp tile with immediate pass 2 (used where consecutive tiles belong to
+// different requests, i.e. the batch kernel).  queue: kTile u32 per warp.
+template <int DIST, bool COUNTED, class Sink>
+__device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, uint64_t seed,
+                                          uint64_t ctr_base, Sink& sink, uint64_t n,
+                                          uint64_t base, uint32_t* queue, int lane,
+                                          LaneCounts& lc) {
+  const uint32_t mask = fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, base, lane, lc);
+  int total;
+  int slot = warp_excl_scan(__popc(mask), lane, &total);
   if (total == 0) return;  // warp-uniform
-  int slot = incl - mine;
-  for (uint32_t m = mask; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    queue[slot++] = (uint16_t)((b / V) * 32 * V + lane * V + (b % V));
-  }
+  for (uint32_t m = mask; m; m &= m - 1)
+    queue[slot++] = mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
   __syncwarp();
-  for (int j0 = 0; j0 < total; j0 += 32) {
-    const int j = j0 + lane;
-    if (j < total) {
-      const uint64_t k = base + queue[j];
-      const uint64_t K = ctr_base + k;
-      const uint64_t u = mix13(seed + (K + 1) * kGamma);
-      CtrStream s{seed + (kExcBase + (K << kExcShift)) * kGamma};
-      double v;
-      if (COUNTED) {
-        Count c;
-        v = draw<DIST>(P, E, u, s, c);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) lc.c[q] += c.c[q];
-      } else {
-        NoCount c;
-        v = draw<DIST>(P, E, u, s, c);
-      }
-      sink.put(k, to_out<OutT>(v), false);
-    }
+  for (int j = lane; j < total; j += 32)
+    resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, base + queue[j], lc);
+  __syncwarp();
+}
+
+// Queue capacity per warp for the cross-tile deferral: < 32 leftovers plus a
+// full tile of exceptions always fit, so no overflow path is needed.
+constexpr int kQueueCap = 32 + kTile;
+
+// A warp's whole share of a fill: tiles first_tile, first_tile + stride, ...
+// Exceptional samples are queued across tiles (entry = tile iteration << 9 |
+// offset) and resolved only in full rounds of 32 -- one per lane -- so pass 2
+// runs with every lane busy instead of once per tile with a few.
+template <int DIST, bool COUNTED, class Sink>
+__device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, uint64_t seed,
+                                          uint64_t ctr_base, Sink& sink, uint64_t n,
+                                          uint64_t first_tile, uint64_t stride, uint32_t* q,
+                                          int lane, LaneCounts& lc) {
+  static_assert(kTile == 512, "entry packing assumes 9 offset bits");
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  int qn = 0;  // warp-uniform queue length
+  auto k_of = [&](uint32_t e) -> uint64_t {
+    return (first_tile + (uint64_t)(e >> 9) * stride) * kTile + (e & 511u);
+  };
+  uint32_t iter = 0;
+  for (uint64_t tile = first_tile; tile < ntiles; tile += stride, ++iter) {
+    const uint32_t mask =
+        fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
+    int total;
+    int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
+    if (total == 0) continue;
+    for (uint32_t m = mask; m; m &= m - 1)
+      q[slot++] = (iter << 9) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
+    qn += total;
+    __syncwarp();
+    if (qn < 32) continue;
+    int done = 0;
+    for (; qn - done >= 32; done += 32)
+      resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
+    __syncwarp();
+    for (int j = lane; j < qn - done; j += 32) q[j] = q[j + done];
+    qn -= done;
+    __syncwarp();
   }
+  if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
   __syncwarp();
 }
 
