@@ -33,9 +33,10 @@ def sources():
     return sorted(list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cpp")))
 
 
-def _compile(src: pathlib.Path) -> tuple[pathlib.Path, str]:
-    obj = OBJ / (src.name + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+def _compile(src: pathlib.Path, obj_dir: pathlib.Path = OBJ,
+             extra: tuple = ()) -> tuple[pathlib.Path, str]:
+    obj = obj_dir / (src.name + ".o")
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cpp":
         cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I",
                str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
@@ -65,6 +66,22 @@ def build(verbose: bool = False) -> pathlib.Path:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
     return LIB
+
+
+def build_variant(name: str, defines: list[str]) -> pathlib.Path:
+    """Experiment builds (e.g. -DZF_MIN_BLOCKS=6) into build/variants/<name>.so;
+    select one at run time with ZF_LIB=<path>."""
+    out_dir = ROOT / "build" / "variants"
+    obj_dir = ROOT / "build" / f"obj_{name}"
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    extra = tuple(f"-D{d}" for d in defines)
+    with cf.ThreadPoolExecutor(max_workers=8) as ex:
+        results = list(ex.map(lambda s: _compile(s, obj_dir, extra), sources()))
+    lib = out_dir / f"{name}.so"
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(lib), *[str(o) for o, _ in results]],
+                   check=True)
+    return lib
 
 
 if __name__ == "__main__":

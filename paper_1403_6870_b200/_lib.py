@@ -9,6 +9,7 @@ the duration of each call, matching the reference's `nogil=True` kernels.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 import threading
 
@@ -16,7 +17,8 @@ import numpy as np
 
 from .errors import DeviceError, ExtensionMissing
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "libzigfast_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get(
+    "ZF_LIB", pathlib.Path(__file__).resolve().parent / "libzigfast_b200.so"))
 
 # constants mirrored from the header
 EXP, NORMAL = 0, 1

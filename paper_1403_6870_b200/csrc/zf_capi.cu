@@ -5,6 +5,7 @@
 // shared by every host thread that targets its device.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 #include <new>
 
@@ -43,6 +44,9 @@ void fill_devpack(const zf_table_pack* p, DevPack* d) {
   d->tailx = p->tailx;
   d->lmax = (int32_t)p->lmax;
   d->nslots = (int32_t)p->nslots;
+  // fast-path sentinel: bytes i >= lmax read sx[i+1] = NaN, so the fast value
+  // of an exceptional word is NaN (the draw bodies never read these entries)
+  for (int i = n; i < (int)(sizeof d->sx / sizeof d->sx[0]); ++i) d->sx[i] = NAN;
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }

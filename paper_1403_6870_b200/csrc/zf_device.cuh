@@ -34,9 +34,10 @@ __host__ __device__ __forceinline__ uint64_t mix13(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// One distribution's pack.  sx has kSlots+1 entries so sx[i+1] is in bounds for
-// every byte i (the fast loop computes it branch-free and discards it when
-// i >= lmax).  Doubles first so every array is 16-byte aligned.
+// One distribution's pack.  sx has kSlots+2 entries so sx[i+1] is in bounds for
+// every byte i: the fast loop reads it branch-free, and entries past L_max hold
+// NaN so an exceptional byte yields a NaN fast value (its detection flag).
+// Doubles first so every array is 16-byte aligned.
 struct alignas(16) DevPack {
   double sx[kSlots + 2];
   double xlo[kSlots];

@@ -1,27 +1,22 @@
-// zf_fill.cu -- production-mode fill: counter-based words, smem tables,
-// warp-deferred exceptional draws, 128-bit coalesced stores.
+// zf_fill.cu -- production-mode fill (zf_fill) and the batched variant.
 //
 // Replaces the hot loops fill_exp (_kernels.py:226-260) and fill_normal
-// (_kernels.py:597-689).  Work decomposition: a persistent grid of 256-thread
-// CTAs; every warp walks "tiles" of 512 consecutive samples (16 per lane).
+// (_kernels.py:597-689) for the counter stream.  Work decomposition: 256-thread
+// CTAs, every warp walks tiles of kTile consecutive samples (zf_tile.cuh):
 //
 //   pass 1 (fast):  lane l, iteration it, element e handles sample
 //                   base + it*32*V + l*V + e   (V = 16 B / sizeof(out))
-//                   -> one splitmix64 word, byte test, one LDS.64 + I2F + DMUL,
-//                   then a 128-bit store per iteration (the warp writes 512
-//                   contiguous bytes per store instruction).  Samples whose
-//                   byte is >= L_max set a bit in a 16-bit lane mask instead.
-//   pass 2 (rare):  the warp compacts the masked samples (popc + shfl scan)
-//                   into a per-warp smem queue and resolves them 32 at a time,
-//                   one per lane, with the full draw body on the sample's
-//                   secondary counter stream; results are patched in with
-//                   8-byte stores to lines that are still resident in L2.
-//
-// Divergence therefore never stalls pass 1: ~1.2-1.6 % of samples take pass 2
-// and a warp runs pass 2 about once per tile, fully packed.
+//                   -> one splitmix64 word, one LDS.64 + I2F + DMUL, then a
+//                   128-bit store per iteration (the warp writes 512 contiguous
+//                   bytes per store instruction).  Exceptional samples are
+//                   flagged by the NaN sentinel of the smem table.
+//   pass 2 (rare):  the flagged samples are queued per warp across tiles and
+//                   resolved 32 at a time (one per lane) on their secondary
+//                   counter streams; results patch lines still held in L2.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "zf_internal.h"
@@ -29,7 +24,16 @@
 
 namespace zf {
 
-template <int DIST, typename OutT, bool COUNTED, bool VEC>
+// Default pass-2 policy per distribution (measured): the
+// exponential's boxes accept ~98.5 % of first attempts, so the uniform
+// speculative round wins; the normal's plain rejection (~59 %) prefers
+// recursive rounds.  Counted fills always use recursive rounds.
+template <int DIST, bool COUNTED>
+constexpr int default_pass2() {
+  return COUNTED ? 3 : (DIST == ZF_EXP ? 5 : 3);
+}
+
+template <int DIST, typename OutT, bool COUNTED, bool VEC, int P2>
 __global__ void __launch_bounds__(kThreads)
     fill_ctr_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
                     OutT* __restrict__ out, uint64_t n, unsigned long long* __restrict__ counters) {
@@ -47,9 +51,9 @@ __global__ void __launch_bounds__(kThreads)
 
   LaneCounts lc;
   StoreSink<OutT, VEC> sink{out};
-  run_tiles<DIST, COUNTED>(P, E, seed, ctr_base, sink, n,
-                           (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
-                           (uint64_t)gridDim.x * kWarps, queue, lane, lc);
+  run_tiles<DIST, COUNTED, P2>(P, E, seed, ctr_base, sink, n,
+                               (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
+                               (uint64_t)gridDim.x * kWarps, queue, lane, lc);
   if (COUNTED) flush_counts(lc, counters);
 }
 
@@ -111,16 +115,37 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
   if (e != cudaSuccess) return (int)e;
   per_sm = std::max(per_sm, 1);
   const uint64_t want = (ntiles + kWarps - 1) / kWarps;
-  *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count);
+  // ZF_GRID_WAVES=w (default 4): w waves of resident CTAs; shorter per-warp
+  // tile runs balance the tail of the launch better than one persistent wave
+  static const int waves = [] {
+    const char* e = getenv("ZF_GRID_WAVES");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count * waves);
   if (*grid < 1) *grid = 1;
   return ZF_OK;
+}
+
+// ZF_PASS2=3|5|9 overrides the pass-2 policy (experiments; 9 is debug-only).
+static int pass2_override() {
+  static const int p = [] {
+    const char* e = getenv("ZF_PASS2");
+    return e ? atoi(e) : 0;
+  }();
+  return p;
 }
 
 template <int DIST, typename OutT, bool COUNTED, bool VEC>
 static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, OutT* out,
                         uint64_t n, unsigned long long* counters, cudaStream_t s) {
-  auto kernel = fill_ctr_kernel<DIST, OutT, COUNTED, VEC>;
   constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  auto kernel = fill_ctr_kernel<DIST, OutT, COUNTED, VEC, default_pass2<DIST, COUNTED>()>;
+  if (!COUNTED) {
+    const int p2 = pass2_override();
+    if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
+    if (p2 == 5) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 5>;
+    if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
+  }
   const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));

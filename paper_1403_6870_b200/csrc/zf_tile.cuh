@@ -1,7 +1,18 @@
 // zf_tile.cuh -- the production warp tile, shared by the fill, batch and
-// generate-and-reduce kernels.  A "sink" decides what happens to each value:
-// StoreSink writes it to HBM (128-bit vector stores in pass 1), StatsSink folds
-// it into per-lane moment sums / histogram / threshold counts without storing.
+// generate-and-reduce kernels.
+//
+// A warp walks "tiles" of kTile consecutive samples (kPerLane per lane).
+//   pass 1  every lane computes the fast-path value of its samples (one
+//           splitmix64 word, LDS.64, I2F, DMUL) and hands V of them at a time
+//           to the sink; exceptional samples (byte >= L_max, ~1.2-1.6 %) only
+//           set a bit in the lane's mask.
+//   pass 2  the warp compacts the masked samples into a per-warp smem queue
+//           that persists across tiles and resolves them in full rounds of 32
+//           (one sample per lane) once 32 are queued.
+// A "sink" decides what happens to each value: StoreSink writes it to HBM
+// (128-bit vector stores in pass 1, 8-byte patches in pass 2 to lines that are
+// still L2-resident), StatsSink folds it into moment sums / histogram /
+// threshold counts without storing anything.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -11,8 +22,17 @@ namespace zf {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPerLane = 16;
-constexpr int kTile = 32 * kPerLane;  // samples per warp tile
+#ifndef ZF_PER_LANE
+#define ZF_PER_LANE 32
+#endif
+constexpr int kPerLane = ZF_PER_LANE;  // samples per lane per tile (<= 32: mask bits)
+constexpr int kTile = 32 * kPerLane;   // samples per warp tile
+constexpr int kTileBits = kTile == 512 ? 9 : kTile == 1024 ? 10 : 8;
+static_assert((1 << kTileBits) == kTile, "tile must be 256, 512 or 1024 samples");
+#ifndef ZF_PASS1_UNROLL
+#define ZF_PASS1_UNROLL 8
+#endif
+constexpr int kPass1Unroll = ZF_PASS1_UNROLL;
 
 template <typename OutT>
 struct VecOf;
@@ -38,7 +58,7 @@ struct StoreSink {
   using Out = OutT;
   static constexpr int V = VecOf<OutT>::V;
   OutT* __restrict__ out;
-  // pass 1: V consecutive values at k (exceptional ones are placeholders,
+  // pass 1: V consecutive values at k (exceptional ones are NaN placeholders,
   // overwritten in pass 2 while the line is still in L2)
   __device__ __forceinline__ void put_vec(uint64_t k, const OutT* v, uint32_t /*exc_bits*/) {
     if constexpr (VEC) {
@@ -85,17 +105,23 @@ struct StatsSink {
   __device__ __forceinline__ void put_vec(uint64_t, const double* v, uint32_t exc_bits) {
 #pragma unroll
     for (int e = 0; e < V; ++e)
-      if (!((exc_bits >> e) & 1)) add(v[e]);
+      if (!((exc_bits >> e) & 1)) add(v[e]);  // bits above V are ignored
   }
   __device__ __forceinline__ void put(uint64_t, double v, bool exc) {
     if (!exc) add(v);
   }
 };
 
-// Pass 1 of one warp tile: samples [base, min(base + kTile, n)) of the
-// counter stream (seed, ctr_base).  Every lane computes the fast-path value of
-// its 16 samples and hands V of them at a time to the sink; returns the lane's
-// mask of exceptional samples (bit it*V + e  <->  offset it*32*V + lane*V + e).
+// mask |= bit if d is NaN (setp.nan on the fp64 pipe + a predicated add)
+__device__ __forceinline__ void or_if_nan(uint32_t& mask, double d, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %1, %1;\n\t@p or.b32 %0, %0, %2;\n\t}"
+      : "+r"(mask)
+      : "d"(d), "r"(bit));
+}
+
+// Pass 1 of one warp tile: samples [base, min(base + kTile, n)) of the counter
+// stream (seed, ctr_base).  Returns the lane's mask of exceptional samples
+// (bit it*V + e  <->  offset it*32*V + lane*V + e).
 template <int DIST, bool COUNTED, class Sink>
 __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, uint64_t ctr_base,
                                               Sink& sink, uint64_t n, uint64_t base, int lane,
@@ -110,19 +136,20 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
   const uint64_t st0 = seed + (ctr_base + k_lane + 1) * kGamma;
   uint32_t mask = 0;
   if (base + kTile <= n) {
-#pragma unroll
+#pragma unroll kPass1Unroll
     for (int it = 0; it < kIters; ++it) {
       const uint64_t st = st0 + (uint64_t)it * kIterStride;
       OutT v[V];
-      uint32_t bits = 0;
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        const uint64_t u = mix13(st + (uint64_t)e * kGamma);
-        bits |= (uint32_t)(((uint32_t)u & 0xFFu) >= lmax) << e;
-        v[e] = to_out<OutT>(fast_value<DIST>(sx, u));
+        // sx[i+1] is NaN for every byte i >= L_max (see fill_devpack), so the
+        // fast value itself flags an exceptional sample: a DSETP on the fp64
+        // pipe instead of integer compare/select work on the busy ALU pipe.
+        const double d = fast_value<DIST>(sx, mix13(st + (uint64_t)e * kGamma));
+        or_if_nan(mask, d, 1u << (it * V + e));
+        v[e] = to_out<OutT>(d);
       }
-      mask |= bits << (it * V);
-      sink.put_vec(k_lane + (uint64_t)it * 32 * V, v, bits);
+      sink.put_vec(k_lane + (uint64_t)it * 32 * V, v, mask >> (it * V));
     }
     if (COUNTED) {
       const unsigned fast = kPerLane - __popc(mask);
@@ -132,7 +159,7 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
   } else {
     // ragged last tile: identical words, bounds-checked element stores
     unsigned valid = 0;
-#pragma unroll
+#pragma unroll 1
     for (int it = 0; it < kIters; ++it) {
 #pragma unroll
       for (int e = 0; e < V; ++e) {
@@ -155,8 +182,8 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
   return mask;
 }
 
-// Pass 2 body for one exceptional sample k: the full draw on its secondary
-// counter stream, written through the sink.
+// Pass 2 body for one exceptional sample k: the full recursive draw on its
+// secondary counter stream, written through the sink.
 template <int DIST, bool COUNTED, class Sink>
 __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, uint64_t seed,
                                             uint64_t ctr_base, Sink& sink, uint64_t k,
@@ -195,8 +222,82 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
   return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
 }
 
-// One warp tile with immediate pass 2 (used where consecutive tiles belong to
-// different requests, i.e. the batch kernel).  queue: kTile u32 per warp.
+// ---------------------------------------------------------------------------
+// Uniform pass 2: one exceptional sample per lane and straight-line code for
+// every lane -- the alias pick and the first box attempt(s) evaluated
+// speculatively from their fixed stream positions (secondary word t of sample
+// K is mix13(st0 + (t+1)*gamma): t = 0,1 alias, then 2 words per attempt), so
+// no lane waits on another lane's rejection loop.  Whatever the straight line
+// cannot finish (the tail slot j = 0, or every speculative attempt rejected) is
+// appended to `slow` and later re-drawn from scratch by resolve_one; the
+// stream is stateless, so the re-draw consumes the same words and yields the
+// same value.  Accept/reject decisions are the reference's own (_kernels.py:
+// 165-180 exponential, :486-494 normal), evaluated in the same order.
+// ---------------------------------------------------------------------------
+template <int DIST>
+struct SpecAttempts {
+  // exponential boxes accept ~98.5 % of attempts; normal boxes ~59 %
+  static constexpr int value = DIST == ZF_EXP ? 1 : 2;
+};
+
+template <int DIST, class Sink, class KOf>
+__device__ __forceinline__ void uniform_round(const DevPack& P, uint64_t seed, uint64_t ctr_base,
+                                              Sink& sink, const uint32_t* q, int cnt, KOf k_of,
+                                              uint32_t* slow, int& slown, int lane) {
+  using OutT = typename Sink::Out;
+  const bool have = lane < cnt;
+  const uint32_t e = q[have ? lane : 0];
+  const uint64_t k = k_of(e);
+  const uint64_t K = ctr_base + k;
+  const uint64_t st = seed + (kExcBase + (K << kExcShift)) * kGamma;
+  const double ua = u01(mix13(st + kGamma));
+  const double ub = u01(mix13(st + 2 * kGamma));
+  const int nsl = P.nslots;
+  long long kk = __double2ll_rz(__dmul_rn(ua, (double)nsl));
+  if (kk >= nsl) kk = nsl - 1;
+  const int j = ub < P.prob[kk] ? (int)kk : P.alias[kk];
+  bool done = false;
+  double v = 0.0;
+#pragma unroll
+  for (int a = 0; a < SpecAttempts<DIST>::value; ++a) {
+    double ux = u01(mix13(st + (uint64_t)(3 + 2 * a) * kGamma));
+    double uy = u01(mix13(st + (uint64_t)(4 + 2 * a) * kGamma));
+    double x, y, arg;
+    bool fast = false;
+    if constexpr (DIST == ZF_EXP) {
+      if (ux > __dsub_rn(1.0, uy)) {
+        const double t = ux;
+        ux = __dsub_rn(1.0, uy);
+        uy = __dsub_rn(1.0, t);
+      }
+      fast = uy < __dsub_rn(__dsub_rn(1.0, ux), P.eps);
+      x = __dadd_rn(P.xlo[j], __dmul_rn(ux, P.xw[j]));  // == (0 + xlo) + ux*xw
+      y = __dadd_rn(P.flo[j], __dmul_rn(uy, P.fh[j]));
+      arg = -x;
+    } else {
+      x = __dadd_rn(P.xlo[j], __dmul_rn(ux, P.xw[j]));
+      y = __dadd_rn(P.flo[j], __dmul_rn(uy, P.fh[j]));
+      arg = __dmul_rn(__dmul_rn(-0.5, x), x);
+    }
+    const bool acc = fast || y < exp(arg);
+    if (!done && acc) v = x;
+    done = done || acc;
+  }
+  done = done && j != 0;
+  if constexpr (DIST == ZF_NORMAL) {
+    const uint64_t u = mix13(seed + (K + 1) * kGamma);  // primary word: the sign
+    if ((long long)u < 0) v = -v;
+  }
+  if (have && done) sink.put(k, to_out<OutT>(v), false);
+  const bool s = have && !done;
+  const unsigned b = __ballot_sync(0xffffffffu, s);
+  if (s) slow[slown + __popc(b & ((1u << lane) - 1u))] = e;
+  slown += __popc(b);
+  __syncwarp();
+}
+
+// One warp tile with its exceptions resolved immediately (the batch kernel,
+// whose consecutive tiles belong to different requests).  queue: kTile u32.
 template <int DIST, bool COUNTED, class Sink>
 __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
@@ -214,47 +315,78 @@ __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, ui
   __syncwarp();
 }
 
-// Queue capacity per warp for the cross-tile deferral: < 32 leftovers plus a
-// full tile of exceptions always fit, so no overflow path is needed.
-constexpr int kQueueCap = 32 + kTile;
+// Per-warp queue words: < 32 leftovers + one full tile, then (uniform policy)
+// the slow queue (< 32 leftovers + one round).
+constexpr int kQueueCap = 32 + kTile + 64;
 
+// Pass-2 policies (template parameter P2 of run_tiles), all bit-identical:
+//   3  rounds of exactly 32 recursive draws as soon as 32 are queued
+//   5  uniform speculative rounds of 32 + a slow queue of recursive rounds
+//   9  DEBUG ONLY: pass 1 alone, exceptions left as NaN (cost isolation)
 // A warp's whole share of a fill: tiles first_tile, first_tile + stride, ...
-// Exceptional samples are queued across tiles (entry = tile iteration << 9 |
-// offset) and resolved only in full rounds of 32 -- one per lane -- so pass 2
-// runs with every lane busy instead of once per tile with a few.
-template <int DIST, bool COUNTED, class Sink>
+// (queue entry = tile iteration << kTileBits | offset within the tile).
+template <int DIST, bool COUNTED, int P2, class Sink>
 __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
                                           uint64_t first_tile, uint64_t stride, uint32_t* q,
                                           int lane, LaneCounts& lc) {
-  static_assert(kTile == 512, "entry packing assumes 9 offset bits");
+  static_assert(P2 == 3 || P2 == 5 || P2 == 9, "unknown pass-2 policy");
+  static_assert(P2 != 5 || !COUNTED, "uniform pass 2 does not keep path counters");
   const uint64_t ntiles = (n + kTile - 1) / kTile;
-  int qn = 0;  // warp-uniform queue length
   auto k_of = [&](uint32_t e) -> uint64_t {
-    return (first_tile + (uint64_t)(e >> 9) * stride) * kTile + (e & 511u);
+    return (first_tile + (uint64_t)(e >> kTileBits) * stride) * kTile + (e & (kTile - 1u));
   };
-  uint32_t iter = 0;
-  for (uint64_t tile = first_tile; tile < ntiles; tile += stride, ++iter) {
-    const uint32_t mask =
-        fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
-    int total;
-    int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
-    if (total == 0) continue;
-    for (uint32_t m = mask; m; m &= m - 1)
-      q[slot++] = (iter << 9) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
-    qn += total;
-    __syncwarp();
-    if (qn < 32) continue;
-    int done = 0;
-    for (; qn - done >= 32; done += 32)
-      resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
-    __syncwarp();
-    for (int j = lane; j < qn - done; j += 32) q[j] = q[j + done];
-    qn -= done;
-    __syncwarp();
+  if constexpr (P2 == 9) {
+    for (uint64_t tile = first_tile; tile < ntiles; tile += stride)
+      fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
+    return;
+  } else {
+    uint32_t* sq = q + 32 + kTile;  // slow queue (policy 5)
+    int qn = 0, sn = 0;            // warp-uniform queue lengths
+    auto drain_slow = [&](bool all) {
+      while (sn >= 32 || (all && sn > 0)) {
+        if (lane < sn) resolve_one<DIST, false>(P, E, seed, ctr_base, sink, k_of(sq[lane]), lc);
+        __syncwarp();
+        const int done = sn < 32 ? sn : 32;
+        for (int j = lane; j < sn - done; j += 32) sq[j] = sq[j + done];
+        sn -= done;
+        __syncwarp();
+      }
+    };
+    uint32_t iter = 0;
+    for (uint64_t tile = first_tile; tile < ntiles; tile += stride, ++iter) {
+      const uint32_t mask =
+          fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
+      int total;
+      int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
+      if (total == 0) continue;
+      for (uint32_t m = mask; m; m &= m - 1)
+        q[slot++] = (iter << kTileBits) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
+      qn += total;
+      __syncwarp();
+      if (qn < 32) continue;
+      int done = 0;
+      for (; qn - done >= 32; done += 32) {
+        if constexpr (P2 == 5) {
+          uniform_round<DIST>(P, seed, ctr_base, sink, q + done, 32, k_of, sq, sn, lane);
+          drain_slow(false);
+        } else {
+          resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
+        }
+      }
+      __syncwarp();
+      for (int j = lane; j < qn - done; j += 32) q[j] = q[j + done];
+      qn -= done;
+      __syncwarp();
+    }
+    if constexpr (P2 == 5) {
+      if (qn) uniform_round<DIST>(P, seed, ctr_base, sink, q, qn, k_of, sq, sn, lane);
+      drain_slow(true);
+    } else {
+      if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
+      __syncwarp();
+    }
   }
-  if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
-  __syncwarp();
 }
 
 __device__ __forceinline__ void flush_counts(const LaneCounts& lc,
