@@ -24,13 +24,11 @@
 
 namespace zf {
 
-// Default pass-2 policy per distribution (measured): the
-// exponential's boxes accept ~98.5 % of first attempts, so the uniform
-// speculative round wins; the normal's plain rejection (~59 %) prefers
-// recursive rounds.  Counted fills always use recursive rounds.
+// Default pass-2 policy (measured): recursive rounds of 32 have
+// the smallest code and register footprint and win for both distributions.
 template <int DIST, bool COUNTED>
 constexpr int default_pass2() {
-  return COUNTED ? 3 : (DIST == ZF_EXP ? 5 : 3);
+  return 3;
 }
 
 template <int DIST, typename OutT, bool COUNTED, bool VEC, int P2>
@@ -126,7 +124,7 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
   return ZF_OK;
 }
 
-// ZF_PASS2=3|5|9 overrides the pass-2 policy (experiments; 9 is debug-only).
+// ZF_PASS2=9 (debug only) runs pass 1 alone to isolate the cost of pass 2.
 static int pass2_override() {
   static const int p = [] {
     const char* e = getenv("ZF_PASS2");
@@ -143,7 +141,6 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
   if (!COUNTED) {
     const int p2 = pass2_override();
     if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
-    if (p2 == 5) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 5>;
     if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
   }
   const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);

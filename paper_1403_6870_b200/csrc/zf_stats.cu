@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   LaneCounts lc;
   const int lane = threadIdx.x & 31;
-  run_tiles<DIST, false, DIST == ZF_EXP ? 5 : 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n,
+  run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n,
                          (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
                          (uint64_t)gridDim.x * kWarps, queue, lane, lc);
   __syncthreads();

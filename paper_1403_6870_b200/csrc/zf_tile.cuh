@@ -222,80 +222,6 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
   return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
 }
 
-// ---------------------------------------------------------------------------
-// Uniform pass 2: one exceptional sample per lane and straight-line code for
-// every lane -- the alias pick and the first box attempt(s) evaluated
-// speculatively from their fixed stream positions (secondary word t of sample
-// K is mix13(st0 + (t+1)*gamma): t = 0,1 alias, then 2 words per attempt), so
-// no lane waits on another lane's rejection loop.  Whatever the straight line
-// cannot finish (the tail slot j = 0, or every speculative attempt rejected) is
-// appended to `slow` and later re-drawn from scratch by resolve_one; the
-// stream is stateless, so the re-draw consumes the same words and yields the
-// same value.  Accept/reject decisions are the reference's own (_kernels.py:
-// 165-180 exponential, :486-494 normal), evaluated in the same order.
-// ---------------------------------------------------------------------------
-template <int DIST>
-struct SpecAttempts {
-  // exponential boxes accept ~98.5 % of attempts; normal boxes ~59 %
-  static constexpr int value = DIST == ZF_EXP ? 1 : 2;
-};
-
-template <int DIST, class Sink, class KOf>
-__device__ __forceinline__ void uniform_round(const DevPack& P, uint64_t seed, uint64_t ctr_base,
-                                              Sink& sink, const uint32_t* q, int cnt, KOf k_of,
-                                              uint32_t* slow, int& slown, int lane) {
-  using OutT = typename Sink::Out;
-  const bool have = lane < cnt;
-  const uint32_t e = q[have ? lane : 0];
-  const uint64_t k = k_of(e);
-  const uint64_t K = ctr_base + k;
-  const uint64_t st = seed + (kExcBase + (K << kExcShift)) * kGamma;
-  const double ua = u01(mix13(st + kGamma));
-  const double ub = u01(mix13(st + 2 * kGamma));
-  const int nsl = P.nslots;
-  long long kk = __double2ll_rz(__dmul_rn(ua, (double)nsl));
-  if (kk >= nsl) kk = nsl - 1;
-  const int j = ub < P.prob[kk] ? (int)kk : P.alias[kk];
-  bool done = false;
-  double v = 0.0;
-#pragma unroll
-  for (int a = 0; a < SpecAttempts<DIST>::value; ++a) {
-    double ux = u01(mix13(st + (uint64_t)(3 + 2 * a) * kGamma));
-    double uy = u01(mix13(st + (uint64_t)(4 + 2 * a) * kGamma));
-    double x, y, arg;
-    bool fast = false;
-    if constexpr (DIST == ZF_EXP) {
-      if (ux > __dsub_rn(1.0, uy)) {
-        const double t = ux;
-        ux = __dsub_rn(1.0, uy);
-        uy = __dsub_rn(1.0, t);
-      }
-      fast = uy < __dsub_rn(__dsub_rn(1.0, ux), P.eps);
-      x = __dadd_rn(P.xlo[j], __dmul_rn(ux, P.xw[j]));  // == (0 + xlo) + ux*xw
-      y = __dadd_rn(P.flo[j], __dmul_rn(uy, P.fh[j]));
-      arg = -x;
-    } else {
-      x = __dadd_rn(P.xlo[j], __dmul_rn(ux, P.xw[j]));
-      y = __dadd_rn(P.flo[j], __dmul_rn(uy, P.fh[j]));
-      arg = __dmul_rn(__dmul_rn(-0.5, x), x);
-    }
-    const bool acc = fast || y < exp(arg);
-    if (!done && acc) v = x;
-    done = done || acc;
-  }
-  done = done && j != 0;
-  if constexpr (DIST == ZF_NORMAL) {
-    const uint64_t u = mix13(seed + (K + 1) * kGamma);  // primary word: the sign
-    if ((long long)u < 0) v = -v;
-  }
-  if (have && done) sink.put(k, to_out<OutT>(v), false);
-  const bool s = have && !done;
-  const unsigned b = __ballot_sync(0xffffffffu, s);
-  if (s) slow[slown + __popc(b & ((1u << lane) - 1u))] = e;
-  slown += __popc(b);
-  __syncwarp();
-}
-
 // One warp tile with its exceptions resolved immediately (the batch kernel,
 // whose consecutive tiles belong to different requests).  queue: kTile u32.
 template <int DIST, bool COUNTED, class Sink>
@@ -315,14 +241,16 @@ __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, ui
   __syncwarp();
 }
 
-// Per-warp queue words: < 32 leftovers + one full tile, then (uniform policy)
-// the slow queue (< 32 leftovers + one round).
-constexpr int kQueueCap = 32 + kTile + 64;
+// Per-warp queue words: < 32 leftovers + one full tile of exceptions.
+constexpr int kQueueCap = 32 + kTile;
 
 // Pass-2 policies (template parameter P2 of run_tiles), all bit-identical:
 //   3  rounds of exactly 32 recursive draws as soon as 32 are queued
-//   5  uniform speculative rounds of 32 + a slow queue of recursive rounds
 //   9  DEBUG ONLY: pass 1 alone, exceptions left as NaN (cost isolation)
+// (Round-1 experiments with uniform speculative rounds, lane-refilling box
+// engines, a resumable state machine and warp specialisation were all
+// bit-identical but slower on B200: their extra registers and code cost the
+// fast path more than they saved.)
 // A warp's whole share of a fill: tiles first_tile, first_tile + stride, ...
 // (queue entry = tile iteration << kTileBits | offset within the tile).
 template <int DIST, bool COUNTED, int P2, class Sink>
@@ -330,8 +258,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
                                           uint64_t first_tile, uint64_t stride, uint32_t* q,
                                           int lane, LaneCounts& lc) {
-  static_assert(P2 == 3 || P2 == 5 || P2 == 9, "unknown pass-2 policy");
-  static_assert(P2 != 5 || !COUNTED, "uniform pass 2 does not keep path counters");
+  static_assert(P2 == 3 || P2 == 9, "unknown pass-2 policy");
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   auto k_of = [&](uint32_t e) -> uint64_t {
     return (first_tile + (uint64_t)(e >> kTileBits) * stride) * kTile + (e & (kTile - 1u));
@@ -341,18 +268,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
     return;
   } else {
-    uint32_t* sq = q + 32 + kTile;  // slow queue (policy 5)
-    int qn = 0, sn = 0;            // warp-uniform queue lengths
-    auto drain_slow = [&](bool all) {
-      while (sn >= 32 || (all && sn > 0)) {
-        if (lane < sn) resolve_one<DIST, false>(P, E, seed, ctr_base, sink, k_of(sq[lane]), lc);
-        __syncwarp();
-        const int done = sn < 32 ? sn : 32;
-        for (int j = lane; j < sn - done; j += 32) sq[j] = sq[j + done];
-        sn -= done;
-        __syncwarp();
-      }
-    };
+    int qn = 0;  // warp-uniform queue length
     uint32_t iter = 0;
     for (uint64_t tile = first_tile; tile < ntiles; tile += stride, ++iter) {
       const uint32_t mask =
@@ -366,26 +282,15 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       __syncwarp();
       if (qn < 32) continue;
       int done = 0;
-      for (; qn - done >= 32; done += 32) {
-        if constexpr (P2 == 5) {
-          uniform_round<DIST>(P, seed, ctr_base, sink, q + done, 32, k_of, sq, sn, lane);
-          drain_slow(false);
-        } else {
-          resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
-        }
-      }
+      for (; qn - done >= 32; done += 32)
+        resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
       __syncwarp();
       for (int j = lane; j < qn - done; j += 32) q[j] = q[j + done];
       qn -= done;
       __syncwarp();
     }
-    if constexpr (P2 == 5) {
-      if (qn) uniform_round<DIST>(P, seed, ctr_base, sink, q, qn, k_of, sq, sn, lane);
-      drain_slow(true);
-    } else {
-      if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
-      __syncwarp();
-    }
+    if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
+    __syncwarp();
   }
 }
 
