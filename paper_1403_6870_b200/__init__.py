@@ -16,6 +16,7 @@ import threading
 
 from .errors import (BitBudgetExceeded, DeviceError, EmptyWeights, ExtensionMissing,
                      FormatError, ZigfastError)
+from .batch import BatchPlan, fill_batch
 from .quality import EXPECTED_MOMENTS, QualityReport, run_quality
 from .samplers import ExpSampler, NormalSampler, PathCounts
 from .tables import (EXPONENTIAL, HALF_NORMAL, AliasTable, ZigguratTables, build_alias,
@@ -55,46 +56,8 @@ def normal(size: int, device=None):
     return _convenience(NormalSampler, size, device)
 
 
-def fill_batch(requests, dtype="float64", device=None):
-    """Many independent production requests in ONE launch (BASELINE config 4).
-
-    ``requests``: iterable of (dist, n, seed) or (dist, n, seed, ctr_base) with
-    dist in {"exp", "normal"}.  Returns one CUDA tensor holding the requests
-    back to back (each padded to a 16-byte boundary) and the offsets.
-    """
-    import ctypes as C
-
-    import torch
-
-    from . import _lib
-    dev = torch.device(device if device is not None else "cuda")
-    if dev.index is None:
-        dev = torch.device("cuda", torch.cuda.current_device())
-    tdtype = torch.float64 if dtype in ("float64", torch.float64) else torch.float32
-    esz = 8 if tdtype == torch.float64 else 4
-    align = 16 // esz
-    reqs = list(requests)
-    arr = (_lib.Request * max(len(reqs), 1))()
-    offsets, off = [], 0
-    for i, r in enumerate(reqs):
-        dist, n, sd = r[0], int(r[1]), int(r[2])
-        base = int(r[3]) if len(r) > 3 else 0
-        arr[i] = _lib.Request(sd & ((1 << 64) - 1), base, n, off,
-                              _lib.EXP if dist in ("exp", "exponential") else _lib.NORMAL, 0)
-        offsets.append(off)
-        off += (n + align - 1) // align * align
-    out = torch.empty(off, dtype=tdtype, device=dev)
-    from .tables import default_tables as _dt
-    tabs = _lib.device_tables(_dt(EXPONENTIAL), _dt(HALF_NORMAL), dev.index)
-    with torch.cuda.device(dev):
-        _lib.check(_lib.lib().zf_fill_batch(tabs.handle, arr, len(reqs),
-                                            _lib.F64 if esz == 8 else _lib.F32, out.data_ptr(),
-                                            _lib.stream_handle(dev)))
-    return out, offsets
-
-
 __all__ = [
-    "AliasTable", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
+    "AliasTable", "BatchPlan", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
     "EmptyWeights", "ExpSampler", "ExtensionMissing", "FormatError", "HALF_NORMAL",
     "NormalSampler", "PathCounts", "QualityReport", "UniformSource", "ZigfastError",
     "ZigguratTables", "auto_seed_value", "build_alias", "default_tables", "derive_seed",

@@ -94,7 +94,17 @@ int zf_tables_create(const zf_table_pack* exp_pack, const zf_table_pack* hn_pack
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) e = cudaMalloc(&t->dev, sizeof(DevTables));
+  if (e == cudaSuccess) {
+    // Oracle-mode scratch comes from the device's stream-ordered pool; keep
+    // freed blocks cached instead of returning them to the driver at every
+    // synchronisation (re-mapping ~1 GB per fill otherwise dominates).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    e = cudaMalloc(&t->dev, sizeof(DevTables));
+  }
   if (e == cudaSuccess) e = cudaMemcpy(t->dev, &t->host, sizeof(DevTables), cudaMemcpyHostToDevice);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {

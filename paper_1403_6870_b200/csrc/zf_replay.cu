@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -412,8 +413,12 @@ static bool debug_on() {
 }
 static void dbg(const char* what, cudaStream_t s) {
   if (!debug_on()) return;
+  static auto last = std::chrono::steady_clock::now();
   cudaError_t e = cudaStreamSynchronize(s);
-  fprintf(stderr, "[zf] %-16s %s\n", what, cudaGetErrorString(e));
+  const auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[zf] %-16s %-10s %8.3f ms\n", what, cudaGetErrorString(e),
+          std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 struct Workspace {

@@ -65,6 +65,19 @@ class PathCounts:
         return self.band_evals / self.box_attempts if self.box_attempts else 0.0
 
 
+_ALIAS_CACHE: dict = {}
+
+
+def _alias_for(tables: ZigguratTables):
+    """The alias table of immutable `tables`, built once per tables object (the
+    reference rebuilds it per sampler, exponential.py:33; same arrays)."""
+    hit = _ALIAS_CACHE.get(id(tables))
+    if hit is None or hit[0] is not tables:
+        hit = (tables, build_alias(tables.a))
+        _ALIAS_CACHE[id(tables)] = hit
+    return hit[1]
+
+
 class _Sampler:
     _dist: int
 
@@ -77,7 +90,7 @@ class _Sampler:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self.tables = tables
         self.exp_tables = exp_tables
-        self.alias = build_alias(tables.a)
+        self.alias = _alias_for(tables)
         self.source = source if source is not None else UniformSource()
         hn = tables if tables.distribution == HALF_NORMAL else default_tables(HALF_NORMAL)
         self._dev_tables = _lib.device_tables(exp_tables, hn, self.device.index)

@@ -1,0 +1,131 @@
+"""Measure the non-headline BASELINE.json configs on one B200 (JSON lines).
+
+    python tools/bench_configs.py [c1 c4 c5 f32 ...]
+
+c1   oracle mode: Exponential / N(0,1) fp64, n = 1e6 from UniformSource(42)
+     (xoshiro256++, the reference's default stream), parallel resolution of the
+     sequential word stream; bit-exactness is asserted by the GPU tests.
+c1big  the same pipeline at n = 2^26 (throughput of oracle mode)
+c4   4096 requests x 8192 samples, alternating exp/normal, seeds 0..4095:
+     one batched launch vs 4096 separate fills
+c5   tail stress, one GPU's share of config 5: N(0,1) n = 2^33, seed 99, counts of
+     |x| > 5, 6, 7 and Exp(1) n = 2^33 counts of x > X[1], vs analytic tail mass
+     (5-sigma binomial); generate-and-count, nothing materialised
+f32  fp32 production fills (n = 2^28) for both distributions
+"""
+import json
+import math
+import sys
+import time
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+import paper_1403_6870_b200 as zf  # noqa: E402
+from paper_1403_6870_b200 import quality  # noqa: E402
+
+dev = torch.device("cuda", 0)
+
+
+def ev_time(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(reps):
+        fn()
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / reps / 1e3  # seconds
+
+
+def wall(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t) / reps
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def c1(n=1_000_000, name="c1"):
+    for dist, cls in (("exp", zf.ExpSampler), ("normal", zf.NormalSampler)):
+        out = torch.empty(n, dtype=torch.float64, device=dev)
+
+        def go():
+            s = cls(source=zf.UniformSource(42), device=dev)
+            s.fill(out)
+        sec = wall(go)
+        emit({"config": name, "dist": dist, "n": n, "mode": "oracle (xoshiro256++ seed 42)",
+              "seconds_per_fill": sec, "samples_per_s": n / sec,
+              "note": "includes device word generation (GF(2) jump-ahead), the parallel "
+                      "replay resolution and the host sync that returns words consumed"})
+
+
+def c4():
+    reqs = [("exp" if i % 2 == 0 else "normal", 8192, i) for i in range(4096)]
+    total = 4096 * 8192
+
+    plan = zf.BatchPlan([d for d, _, _ in reqs], [n for _, n, _ in reqs],
+                        [sd for _, _, sd in reqs])
+    buf = plan.fill(device=dev)
+    sec_b = wall(lambda: plan.fill(buf, device=dev), reps=10)
+    sec_k = ev_time(lambda: plan.fill(buf, device=dev), reps=20)
+    outs = torch.empty(total, dtype=torch.float64, device=dev)
+
+    def separate():
+        for i, (d, n, sd) in enumerate(reqs):
+            cls = zf.ExpSampler if d == "exp" else zf.NormalSampler
+            cls(source=zf.UniformSource.counter(sd), device=dev).fill(outs[i * n:(i + 1) * n])
+    sec_s = wall(separate, reps=1)
+    emit({"config": "c4", "requests": 4096, "per_request": 8192,
+          "batched_seconds": sec_b, "batched_samples_per_s": total / sec_b,
+          "batched_event_seconds": sec_k, "batched_event_samples_per_s": total / sec_k,
+          "separate_seconds": sec_s, "separate_samples_per_s": total / sec_s,
+          "note": "batched = one zf_fill_batch launch incl. request-table upload; separate = "
+                  "4096 sampler constructions + fills through the Python API"})
+
+
+def c5(n=1 << 33):
+    s = zf.NormalSampler(source=zf.UniformSource.counter(99), device=dev)
+    t = time.perf_counter()
+    _, res = quality.device_sums(s, n, thresholds=(5.0, 6.0, 7.0), abs_thresh=True)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t
+    rows = []
+    for th, c in zip((5.0, 6.0, 7.0), res.thresh_counts):
+        p = math.erfc(th / math.sqrt(2.0))
+        ok, mean, sd = quality.binomial_check(c, n, p)
+        rows.append({"threshold": th, "count": c, "expected": mean, "sd": sd, "within_5sigma": ok})
+    x1 = float(zf.default_tables("exponential").x[1])
+    se = zf.ExpSampler(source=zf.UniformSource.counter(99), device=dev)
+    _, rese = quality.device_sums(se, n, thresholds=(x1,))
+    ok, mean, sd = quality.binomial_check(rese.thresh_counts[0], n, math.exp(-x1))
+    emit({"config": "c5 (one GPU's share: 2^33 of 2^36)", "n": n, "seconds_normal": sec,
+          "samples_per_s_generate_and_count": n / sec, "normal_tails": rows,
+          "exp_tail_beyond_X1": {"X1": x1, "count": rese.thresh_counts[0], "expected": mean,
+                                 "sd": sd, "within_5sigma": ok}})
+
+
+def f32(n=1 << 28):
+    for dist, cls in (("exp", zf.ExpSampler), ("normal", zf.NormalSampler)):
+        s = cls(source=zf.UniformSource.counter(1234), device=dev)
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+        sec = ev_time(lambda: s.fill(out))
+        emit({"config": "f32", "dist": dist, "n": n, "samples_per_s": n / sec,
+              "gbs": 4 * n / sec / 1e9})
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1", "c1big", "c4", "c5", "f32"]
+    for w in which:
+        if w == "c1big":
+            c1(1 << 26, "c1big")
+        else:
+            globals()[w]()

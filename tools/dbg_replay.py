@@ -1,12 +1,14 @@
-import faulthandler, sys, time
-faulthandler.dump_traceback_later(40, exit=True)
+"""ZF_DEBUG=1 python tools/dbg_replay.py [normal|exp] [log2 n]: per-stage replay timings."""
+import sys
 sys.path.insert(0, '.')
-import torch, numpy as np
+import torch
 import paper_1403_6870_b200 as zf
+dist = sys.argv[1] if len(sys.argv) > 1 else "normal"
+n = 1 << int(sys.argv[2] if len(sys.argv) > 2 else 26)
+cls = zf.NormalSampler if dist == "normal" else zf.ExpSampler
 dev = torch.device('cuda', 0)
-print('start', flush=True)
-s = zf.ExpSampler(source=zf.UniformSource.replay([123456789 << 8]), device=dev)
-print('sampler ok', flush=True)
-t = time.time(); print(s.sample(), time.time() - t, flush=True)
-s = zf.ExpSampler(source=zf.UniformSource(7), device=dev)
-t = time.time(); print(s.fill(5), time.time() - t, flush=True)
+out = torch.empty(n, dtype=torch.float64, device=dev)
+for _ in range(2):
+    cls(source=zf.UniformSource(42), device=dev).fill(out)
+    torch.cuda.synchronize()
+    print("---", flush=True)
