@@ -31,8 +31,12 @@ constexpr int default_pass2() {
   return 3;
 }
 
+#ifndef ZF_MIN_BLOCKS
+#define ZF_MIN_BLOCKS 1  // CTAs per SM requested from the register allocator
+#endif
+
 template <int DIST, typename OutT, bool COUNTED, bool VEC, int P2>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
     fill_ctr_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
                     OutT* __restrict__ out, uint64_t n, unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(kThreads)
   stage_block(st, gt, (int)sizeof(DevTables));
   const int lane = threadIdx.x & 31;
   uint32_t* queue =
-      reinterpret_cast<uint32_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kTile;
+      reinterpret_cast<uint32_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kQueueCap;
   __syncthreads();
   LaneCounts lc;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
@@ -90,11 +94,11 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t base = (tile - r.tile_begin) * kTile;
     StoreSink<OutT, VEC> sink{out + r.out_offset};
     if (r.dist == ZF_EXP)
-      fill_tile<ZF_EXP, false>(st->ex, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue, lane,
-                               lc);
+      fill_tile<ZF_EXP, false>(st->ex, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue,
+                               kQueueCap, lane, lc);
     else
       fill_tile<ZF_NORMAL, false>(st->hn, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue,
-                                  lane, lc);
+                                  kQueueCap, lane, lc);
   }
 }
 
@@ -181,7 +185,7 @@ template <typename OutT, bool VEC>
 static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq, int nreq,
                               uint64_t total_tiles, OutT* out, cudaStream_t s) {
   auto kernel = fill_batch_kernel<OutT, VEC>;
-  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kTile * sizeof(uint32_t);
+  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_tiles, &grid));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, nreq, total_tiles, out);

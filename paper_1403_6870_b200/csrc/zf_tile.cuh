@@ -223,16 +223,23 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
 }
 
 // One warp tile with its exceptions resolved immediately (the batch kernel,
-// whose consecutive tiles belong to different requests).  queue: kTile u32.
+// whose consecutive tiles belong to different requests).  queue: cap u32.
 template <int DIST, bool COUNTED, class Sink>
 __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
-                                          uint64_t base, uint32_t* queue, int lane,
+                                          uint64_t base, uint32_t* queue, int cap, int lane,
                                           LaneCounts& lc) {
   const uint32_t mask = fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, base, lane, lc);
   int total;
   int slot = warp_excl_scan(__popc(mask), lane, &total);
   if (total == 0) return;  // warp-uniform
+  if (total > cap) {  // (practically never) resolve in place from the lane masks
+    for (uint32_t m = mask; m; m &= m - 1)
+      resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink,
+                                 base + mask_bit_offset<Sink::V>(__ffs(m) - 1, lane), lc);
+    __syncwarp();
+    return;
+  }
   for (uint32_t m = mask; m; m &= m - 1)
     queue[slot++] = mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
   __syncwarp();
@@ -241,8 +248,13 @@ __device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, ui
   __syncwarp();
 }
 
-// Per-warp queue words: < 32 leftovers + one full tile of exceptions.
-constexpr int kQueueCap = 32 + kTile;
+// Per-warp queue words: < 32 leftovers + the exceptions of one tile (~15 on
+// average for 1024 samples); a tile that would overflow is resolved in place.
+// Small on purpose: shared memory, not registers, limits CTAs per SM.
+#ifndef ZF_QUEUE_CAP
+#define ZF_QUEUE_CAP 128
+#endif
+constexpr int kQueueCap = ZF_QUEUE_CAP;
 
 // Pass-2 policies (template parameter P2 of run_tiles), all bit-identical:
 //   3  rounds of exactly 32 recursive draws as soon as 32 are queued
@@ -276,6 +288,16 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       int total;
       int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
       if (total == 0) continue;
+      if (qn + total > kQueueCap) {
+        // (practically never: ~100 exceptions in one tile, expected ~15) resolve
+        // this tile's exceptions in place, each lane walking its own mask
+        for (uint32_t m = mask; m; m &= m - 1)
+          resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink,
+                                     tile * kTile + mask_bit_offset<Sink::V>(__ffs(m) - 1, lane),
+                                     lc);
+        __syncwarp();
+        continue;
+      }
       for (uint32_t m = mask; m; m &= m - 1)
         q[slot++] = (iter << kTileBits) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
       qn += total;
