@@ -23,7 +23,7 @@ namespace zf {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 #ifndef ZF_PER_LANE
-#define ZF_PER_LANE 32
+#define ZF_PER_LANE 16
 #endif
 constexpr int kPerLane = ZF_PER_LANE;  // samples per lane per tile (<= 32: mask bits)
 constexpr int kTile = 32 * kPerLane;   // samples per warp tile
@@ -189,6 +189,10 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
                                             uint64_t ctr_base, Sink& sink, uint64_t k,
                                             LaneCounts& lc) {
   using OutT = typename Sink::Out;
+#if defined(ZF_DEBUG_P2) && ZF_DEBUG_P2 == 2  // cost isolation: store without drawing
+  sink.put(k, to_out<OutT>(0.0), false);
+  return;
+#endif
   const uint64_t K = ctr_base + k;
   const uint64_t u = mix13(seed + (K + 1) * kGamma);
   CtrStream s{seed + (kExcBase + (K << kExcShift)) * kGamma};
@@ -202,6 +206,10 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
     NoCount c;
     v = draw<DIST>(P, E, u, s, c);
   }
+#if defined(ZF_DEBUG_P2) && ZF_DEBUG_P2 == 1  // cost isolation: draw without storing
+  if (v == 12345.0) sink.put(k, to_out<OutT>(v), false);
+  return;
+#endif
   sink.put(k, to_out<OutT>(v), false);
 }
 
