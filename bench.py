@@ -181,7 +181,7 @@ def run_reference(args, rank: int):
     threads = cpu_threads()
     import numpy as np
     from oracle import oracle
-    n = max(threads << 20, 1 << 22)  # bounded per-step sample
+    n = max(threads << 22, 1 << 24)  # bounded per-step sample (~tens of ms of CPU work)
     buf = np.empty(n)
     for _ in range(args.warmup):
         oracle.fill_sharded("normal", n, SEED, threads=threads, out=buf)
