@@ -529,7 +529,13 @@ template <int DIST, typename OutT>
 int replay_typed(const zf_tables* t, const uint64_t* words, uint64_t nwords, uint64_t cursor,
                  int wrap, void* out, uint64_t n, zf_path_rec* recs, int64_t* counters,
                  uint64_t* consumed, cudaStream_t s) {
-  const uint64_t cap = wrap ? (1ull << 32) - kRB : nwords - std::min(cursor, nwords);
+  // A window of 2n + 2^20 words is never needed by a random stream (draws take
+  // ~1.06 words on average); a replay list whose draws cycle forever (possible
+  // with short wrapping lists -- the reference would loop without end) is
+  // reported as ZF_ERANGE instead of growing the window towards 2^32.
+  const uint64_t sane = 2 * n + (1ull << 20);
+  const uint64_t cap = std::min<uint64_t>(
+      sane, wrap ? (1ull << 32) - kRB : nwords - std::min(cursor, nwords));
   uint64_t L = std::min<uint64_t>(cap, n + n / 8 + 4096);
   for (;;) {
     if (L == 0) return ZF_ESHORT;
@@ -537,7 +543,7 @@ int replay_typed(const zf_tables* t, const uint64_t* words, uint64_t nwords, uin
     bool retry = false;
     ZF_TRY_STATUS((replay_window<DIST, OutT>(t, win, out, n, recs, counters, consumed, &retry, s)));
     if (!retry) return ZF_OK;
-    if (L >= cap) return wrap ? ZF_ERANGE : ZF_ESHORT;
+    if (L >= cap) return (wrap || cap == sane) ? ZF_ERANGE : ZF_ESHORT;
     L = std::min<uint64_t>(cap, 2 * L);
   }
 }

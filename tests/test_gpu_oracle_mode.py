@@ -158,3 +158,14 @@ def test_adversarial_replay_all_exceptional(zf, orc, cuda):
         want, _, _, used = orc.fill_stream(dist, 3000, replay_words=words)
         assert np.array_equal(bits(got), bits(want)), dist
         assert int(s.source.state[0]) == used
+
+
+def test_cycling_replay_is_an_error_not_a_hang(zf, cuda):
+    """A short wrapping list on which a normal-tail draw can never finish (the
+    reference would loop forever) fails with ZF_ERANGE instead of hanging."""
+    from paper_1403_6870_b200.errors import DeviceError
+    s = zf.NormalSampler(source=zf.UniformSource.replay([255, 0, 0, 123456789 << 8, 7]),
+                         device=cuda)
+    with pytest.raises(DeviceError) as ei:
+        s.fill(100)
+    assert ei.value.status == -4

@@ -144,3 +144,63 @@ def test_convenience_api(zf, cuda):
     assert np.array_equal(bits(np.concatenate([a.cpu().numpy(), b.cpu().numpy()])),
                           bits(c.cpu().numpy()))
     assert zf.exponential(10, device=cuda).min().item() > 0.0
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_full_size_fill_properties(zf, orc, cuda, dist):
+    """BASELINE config 3 size on one GPU (n = 2^32 + 77, 32 GiB): spot-check
+    windows against the oracle at arbitrary offsets, and size-independent
+    properties (finite, sign/positivity, moments within 6 sigma)."""
+    import torch
+    from paper_1403_6870_b200 import quality
+    n = (1 << 32) + 77
+    free, _ = torch.cuda.mem_get_info(cuda)
+    if free < 8 * n + (4 << 30):
+        pytest.skip("not enough device memory")
+    s = sampler(zf, dist, 7, 1 << 40, device=cuda)
+    out = s.fill(n)
+    for off in (0, 12345, (1 << 31) + 3, n - 1000):
+        want, _, _ = orc.fill_ctr(dist, 1000, seed=7, ctr_base=(1 << 40) + off)
+        assert np.array_equal(bits(out[off:off + 1000].cpu().numpy()), bits(want)), off
+    sums, res = quality.buffer_sums(out, thresholds=(0.0,))
+    raw = [v / n for v in sums]
+    if dist == "normal":
+        mean, var, skew, exk = quality.central_moments_from_raw(raw)
+        for val, se in ((mean, (1 / n) ** 0.5), (var - 1, (2 / n) ** 0.5),
+                        (skew, (6 / n) ** 0.5), (exk, (24 / n) ** 0.5)):
+            assert abs(val / se) < 6.0
+        assert abs(res.thresh_counts[0] - n / 2) < 6 * (n / 4) ** 0.5
+    else:
+        assert res.thresh_counts[0] == n  # every draw > 0
+        for k, want in enumerate((1.0, 2.0)):
+            sd = quality._MOMENT_SD["exp"][k] / n ** 0.5
+            assert abs(raw[k] - want) < 6 * sd
+    assert torch.isfinite(out).all().item()
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_concurrent_host_threads(zf, orc, cuda):
+    """Samplers are single-owner, the uploaded tables are shared: several host
+    threads filling on their own streams give the same bits as serial fills."""
+    import threading
+
+    import torch
+    results = {}
+
+    def work(i):
+        st = torch.cuda.Stream(cuda)
+        with torch.cuda.stream(st):
+            s = sampler(zf, "normal" if i % 2 else "exp", 100 + i, device=cuda)
+            v = s.fill(200_000)
+        st.synchronize()
+        results[i] = v.cpu().numpy()
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for i in range(6):
+        want, _, _ = orc.fill_ctr("normal" if i % 2 else "exp", 200_000, seed=100 + i)
+        assert np.array_equal(bits(results[i]), bits(want)), i
