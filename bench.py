@@ -74,26 +74,36 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self._stop = index, [], threading.Event()
+        self._ready = threading.Event()
+        self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run(self):
+    def _init_nvml(self):
         try:  # in-process NVML: ~microseconds per sample, so short regions get many
             import pynvml as N
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.index)
             bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
                     N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
-            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self._nvml = (N, h, bits, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        N, h, bits, mx = self._nvml
+        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append([str(self.index), str(sm), str(mx), f"{pw:.1f}"] +
+                         ["Active" if r & b else "Not Active" for b in bits])
+
+    def _run(self):
+        if self._nvml:
             while not self._stop.is_set():
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append([str(self.index), str(sm), str(mx), f"{pw:.1f}"] +
-                                 ["Active" if r & b else "Not Active" for b in bits])
+                self._sample_nvml()
+                self._ready.set()
                 self._stop.wait(0.002)
             return
-        except Exception:
-            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -103,15 +113,20 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
+        self._init_nvml()  # before the timed region starts
         self._t.start()
+        self._ready.wait(timeout=10)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nvml:  # one more sample at the end of the region
+            self._sample_nvml()
 
     def summary(self):
         if not self.rows:
@@ -218,6 +233,34 @@ def time_fill(sampler, out, steps: int, warmup: int, stream):
     return t0.elapsed_time(t1) / steps  # ms per launch (one kernel per step)
 
 
+def time_aggregate(sampler, n: int, steps: int, warmup: int, stream):
+    """Device time of the fused generate-and-sum kernel (sum of n draws, no
+    HBM writes) -- the reference's own bench loop, `_kernels.py:703-922`."""
+    import ctypes as C
+
+    import torch
+    from paper_1403_6870_b200 import _lib, quality
+    cfg = quality._cfg(moments=1)
+    partials, counts = quality._buffers(sampler.device, n, cfg)
+    lib = _lib.lib()
+    src = sampler.source
+
+    def one():
+        _lib.check(lib.zf_fill_stats(sampler._dev_tables.handle, sampler._dist,
+                                     int(src.state[0]), int(src.state[1]), n, C.byref(cfg),
+                                     partials.data_ptr(), counts.data_ptr(), stream.cuda_stream))
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / steps
+
+
 def write_peak(buf, reps: int = 10):
     """Write-only HBM bandwidth on this GPU: torch fill_ (a pure store kernel)."""
     import torch
@@ -263,6 +306,7 @@ def main():
 
     # exponential leg first (reported beside the headline)
     exp_ms = time_fill(expo, out, args.steps, args.warmup, stream)
+    agg_ms = time_aggregate(normal, n, args.steps, args.warmup, stream)
 
     # headline: normal, with clocks sampled during the timed region
     for _ in range(args.warmup):
@@ -281,10 +325,10 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    ms_all = torch.tensor([ms, exp_ms], dtype=torch.float64, device=dev)
+    ms_all = torch.tensor([ms, exp_ms, agg_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_all, op=dist.ReduceOp.MAX)
-    ms_max, exp_ms_max = ms_all.tolist()
+    ms_max, exp_ms_max, agg_ms_max = ms_all.tolist()
 
     # validation of the last step's output; only these sums cross NCCL
     sums, res = quality.buffer_sums(out, hist=(-6.0, 6.0, 1024), thresholds=(5.0, 6.0, 7.0),
@@ -346,6 +390,10 @@ def main():
                        "l2": "output 2 GiB per step > 126 MB L2 (no flush needed)",
                        "parallelism": f"dp{world} (disjoint counter ranges, no hot-path collective)"},
             "exp_value": n * world / (exp_ms_max * 1e-3), "exp_ms_per_step": exp_ms_max,
+            "aggregate": {"value": n * world / (agg_ms_max * 1e-3), "unit": UNIT,
+                          "ms_per_step": agg_ms_max, "kernel": "fill_stats_kernel<normal,sum>",
+                          "note": "generate-and-sum of the same n draws, nothing written "
+                                  "(the reference's aggregate / bench loop)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_sample": 8, "write_peak_gbs": wp,
@@ -358,7 +406,7 @@ def main():
                            "tail_counts_abs_gt_5_6_7": v[5 + 1026:5 + 1029],
                            "allreduce": "nccl" if world > 1 else "none"},
             "clocks": clk.summary(),
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps,  # one fill_ctr_kernel launch per timed step
             "e2e": e2e,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -108,7 +108,8 @@ typedef struct zf_stats_cfg {
   int32_t nbins;      /* 0 disables the histogram; counts has nbins + 2 slots (under, over) */
   int32_t nthresh;    /* <= 8 */
   int32_t abs_thresh; /* count |x| > t instead of x > t */
-  int32_t reserved;
+  int32_t moments;    /* 0 or 5: x^1..x^5; 1 with no histogram/thresholds: the
+                         sum only (aggregate, _kernels.py:306-393) */
   double thresh[8];
 } zf_stats_cfg;
 

@@ -50,7 +50,7 @@ class Request(C.Structure):
 
 class StatsCfg(C.Structure):
     _fields_ = [("hist_lo", C.c_double), ("hist_hi", C.c_double), ("nbins", C.c_int32),
-                ("nthresh", C.c_int32), ("abs_thresh", C.c_int32), ("reserved", C.c_int32),
+                ("nthresh", C.c_int32), ("abs_thresh", C.c_int32), ("moments", C.c_int32),
                 ("thresh", C.c_double * 8)]
 
 

@@ -20,26 +20,38 @@ namespace {
 constexpr uint32_t kMaxStatBlocks = 148 * 8;
 constexpr int kMaxBins = 4096;
 
+// Block scratch; the histogram (nbins + 2 u32) follows it in dynamic shared
+// memory only when enabled, so moment-only reductions keep full occupancy.
 struct StatsShared {
   double thresh[8];
-  unsigned int hist[kMaxBins + 2];
   double warp_sums[kWarps][5];
 };
 
-__device__ void init_sink(StatsSink& k, StatsShared* sh, const zf_stats_cfg& cfg) {
-  for (int i = threadIdx.x; i < cfg.nbins + 2; i += blockDim.x) sh->hist[i] = 0;
-  if (threadIdx.x < 8) sh->thresh[threadIdx.x] = cfg.thresh[threadIdx.x];
-  k.hist = sh->hist;
+template <bool EXTRA>
+__device__ void init_sink(StatsSinkT<EXTRA>& k, StatsShared* sh, unsigned int* hist,
+                          const zf_stats_cfg& cfg) {
+  if (cfg.nbins)  // hist has nbins + 2 slots only when the histogram is enabled
+    for (int i = threadIdx.x; i < cfg.nbins + 2; i += blockDim.x) hist[i] = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)  // static indices: the param struct stays out of local memory
+    if (threadIdx.x == q) sh->thresh[q] = cfg.thresh[q];
+  k.hist = hist;
   k.lo = cfg.hist_lo;
   k.inv_w = cfg.nbins ? (double)cfg.nbins / (cfg.hist_hi - cfg.hist_lo) : 0.0;
   k.nbins = cfg.nbins;
   k.nthresh = cfg.nthresh;
   k.abs_t = cfg.abs_thresh != 0;
   k.t = sh->thresh;
+  k.tmin = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < cfg.nthresh) k.tmin = fmin(k.tmin, cfg.thresh[q]);
 }
 
-__device__ void flush_sink(const StatsSink& k, StatsShared* sh, const zf_stats_cfg& cfg,
-                           double* __restrict__ partials, unsigned long long* __restrict__ counts) {
+template <bool EXTRA>
+__device__ void flush_sink(const StatsSinkT<EXTRA>& k, StatsShared* sh, const unsigned int* hist,
+                           const zf_stats_cfg& cfg, double* __restrict__ partials,
+                           unsigned long long* __restrict__ counts) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int q = 0; q < 5; ++q) {
     double v = k.s[q];
@@ -47,7 +59,9 @@ __device__ void flush_sink(const StatsSink& k, StatsShared* sh, const zf_stats_c
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     if (lane == 0) sh->warp_sums[wid][q] = v;
   }
-  for (int q = 0; q < cfg.nthresh; ++q) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (!EXTRA || q >= cfg.nthresh) break;
     unsigned long long v = k.thr[q];
 #pragma unroll
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -59,11 +73,29 @@ __device__ void flush_sink(const StatsSink& k, StatsShared* sh, const zf_stats_c
     for (int w = 0; w < kWarps; ++w) acc += sh->warp_sums[w][threadIdx.x];
     partials[(uint64_t)blockIdx.x * 5 + threadIdx.x] = acc;
   }
-  for (int i = threadIdx.x; i < cfg.nbins + 2; i += blockDim.x)
-    if (sh->hist[i]) atomicAdd(counts + i, (unsigned long long)sh->hist[i]);
+  if (cfg.nbins)
+    for (int i = threadIdx.x; i < cfg.nbins + 2; i += blockDim.x)
+      if (hist[i]) atomicAdd(counts + i, (unsigned long long)hist[i]);
 }
 
-template <int DIST>
+// Sum-only flush: lanes -> warps (shuffle tree) -> block row [sum, 0, 0, 0, 0].
+__device__ void flush_sum(double v, StatsShared* sh, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  if (lane == 0) sh->warp_sums[wid][0] = v;
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double acc = 0.0;
+    if (threadIdx.x == 0)
+      for (int w = 0; w < kWarps; ++w) acc += sh->warp_sums[w][0];
+    partials[(uint64_t)blockIdx.x * 5 + threadIdx.x] = acc;
+  }
+}
+
+// MODE 0: the aggregate (moments == 1, no histogram, no thresholds);
+// 1: moments x^1..x^5 only; 2: moments + histogram + threshold counts.
+template <int DIST, int MODE>
 __global__ void __launch_bounds__(kThreads)
     fill_stats_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
                       uint64_t n, zf_stats_cfg cfg, double* __restrict__ partials,
@@ -72,34 +104,62 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
   StatsShared* sh = reinterpret_cast<StatsShared*>(smem_raw + kPacks * sizeof(DevPack));
-  uint32_t* queue = reinterpret_cast<uint32_t*>(sh + 1) + (threadIdx.x >> 5) * kQueueCap;
+  uint32_t* queues = reinterpret_cast<uint32_t*>(sh + 1);
+  uint32_t* queue = queues + (threadIdx.x >> 5) * kQueueCap;
+  unsigned int* hist = queues + kWarps * kQueueCap;
   stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
               kPacks * (int)sizeof(DevPack));
-  StatsSink sink;
-  init_sink(sink, sh, cfg);
-  __syncthreads();
-  LaneCounts lc;
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const int lane = threadIdx.x & 31;
-  run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n,
-                         (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
-                         (uint64_t)gridDim.x * kWarps, queue, lane, lc);
-  __syncthreads();
-  flush_sink(sink, sh, cfg, partials, counts);
+  LaneCounts lc;
+  if constexpr (MODE == 0) {
+    __syncthreads();
+    SumSink sink;
+    run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
+                              queue, lane, lc);
+    flush_sum(sink.s, sh, partials);
+  } else {
+    StatsSinkT<MODE == 2> sink;
+    init_sink(sink, sh, hist, cfg);
+    __syncthreads();
+    run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
+                              queue, lane, lc);
+    __syncthreads();
+    flush_sink(sink, sh, hist, cfg, partials, counts);
+  }
 }
 
-template <typename T>
+// Buffer statistics: 16-byte loads, grid-stride over vector slots.
+template <typename T, bool EXTRA>
 __global__ void __launch_bounds__(kThreads)
     stats_kernel(const T* __restrict__ x, uint64_t n, zf_stats_cfg cfg,
                  double* __restrict__ partials, unsigned long long* __restrict__ counts) {
-  __shared__ StatsShared sh;
-  StatsSink sink;
-  init_sink(sink, &sh, cfg);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StatsShared* sh = reinterpret_cast<StatsShared*>(smem_raw);
+  unsigned int* hist = reinterpret_cast<unsigned int*>(sh + 1);
+  StatsSinkT<EXTRA> sink;
+  init_sink(sink, sh, hist, cfg);
   __syncthreads();
+  using Vec = typename VecOf<T>::T;
+  constexpr int V = VecOf<T>::V;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    sink.add((double)x[i]);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t head = std::min<uint64_t>(n, (16 - (reinterpret_cast<uintptr_t>(x) & 15)) % 16 / sizeof(T));
+  if (tid < head) sink.add((double)x[tid]);
+  const T* xa = x + head;
+  const uint64_t nv = (n - head) / V;
+  const Vec* xv = reinterpret_cast<const Vec*>(xa);
+#pragma unroll 4
+  for (uint64_t i = tid; i < nv; i += stride) {
+    const Vec w = __ldcs(xv + i);
+    const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int j = 0; j < V; ++j) sink.add((double)e[j]);
+  }
+  for (uint64_t i = head + nv * V + tid; i < n; i += stride) sink.add((double)x[i]);
   __syncthreads();
-  flush_sink(sink, &sh, cfg, partials, counts);
+  flush_sink(sink, sh, hist, cfg, partials, counts);
 }
 
 int check_cfg(const zf_stats_cfg* cfg) {
@@ -107,7 +167,33 @@ int check_cfg(const zf_stats_cfg* cfg) {
   if (cfg->nbins < 0 || cfg->nbins > kMaxBins || cfg->nthresh < 0 || cfg->nthresh > 8)
     return ZF_EINVAL;
   if (cfg->nbins && !(cfg->hist_hi > cfg->hist_lo)) return ZF_EINVAL;
+  if (cfg->moments < 0 || cfg->moments > 5) return ZF_EINVAL;
   return ZF_OK;
+}
+
+bool extra(const zf_stats_cfg* cfg) { return cfg->nbins != 0 || cfg->nthresh != 0; }
+bool sum_only(const zf_stats_cfg* cfg) { return cfg->moments == 1 && !extra(cfg); }
+
+size_t hist_bytes(const zf_stats_cfg* cfg) {
+  return cfg->nbins ? ((size_t)(cfg->nbins + 2) * sizeof(unsigned int) + 15) / 16 * 16 : 0;
+}
+
+
+template <int DIST>
+int launch_fill_stats_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base, uint64_t n,
+                           const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,
+                           cudaStream_t s) {
+  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  const uint32_t grid = stats_blocks(n);
+  const int mode = sum_only(cfg) ? 0 : extra(cfg) ? 2 : 1;
+  const size_t smem = kPacks * sizeof(DevPack) + sizeof(StatsShared) +
+                      (size_t)kWarps * kQueueCap * sizeof(uint32_t) + hist_bytes(cfg);
+  auto kern = mode == 0   ? fill_stats_kernel<DIST, 0>
+              : mode == 1 ? fill_stats_kernel<DIST, 1>
+                          : fill_stats_kernel<DIST, 2>;
+  ZF_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, n, *cfg, partials, counts);
+  return cuda_status(cudaGetLastError());
 }
 
 }  // namespace
@@ -121,36 +207,25 @@ int launch_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_
                       const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,
                       cudaStream_t s) {
   ZF_TRY_STATUS(check_cfg(cfg));
-  const uint32_t grid = stats_blocks(n);
-  const size_t queue = (size_t)kWarps * kQueueCap * sizeof(uint32_t);
-  if (dist == ZF_EXP) {
-    const size_t smem = sizeof(DevPack) + sizeof(StatsShared) + queue;
-    ZF_TRY(cudaFuncSetAttribute(fill_stats_kernel<ZF_EXP>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fill_stats_kernel<ZF_EXP><<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, n, *cfg,
-                                                           partials, counts);
-  } else if (dist == ZF_NORMAL) {
-    const size_t smem = 2 * sizeof(DevPack) + sizeof(StatsShared) + queue;
-    ZF_TRY(cudaFuncSetAttribute(fill_stats_kernel<ZF_NORMAL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fill_stats_kernel<ZF_NORMAL><<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, n, *cfg,
-                                                              partials, counts);
-  } else {
-    return ZF_EDIST;
-  }
-  return cuda_status(cudaGetLastError());
+  if (dist == ZF_EXP)
+    return launch_fill_stats_dist<ZF_EXP>(t, seed, ctr_base, n, cfg, partials, counts, s);
+  if (dist == ZF_NORMAL)
+    return launch_fill_stats_dist<ZF_NORMAL>(t, seed, ctr_base, n, cfg, partials, counts, s);
+  return ZF_EDIST;
 }
 
 int launch_stats(int dtype, const void* x, uint64_t n, const zf_stats_cfg* cfg, double* partials,
                  unsigned long long* counts, cudaStream_t s) {
   ZF_TRY_STATUS(check_cfg(cfg));
   const uint32_t grid = stats_blocks(n);
+  const size_t smem = sizeof(StatsShared) + hist_bytes(cfg);
+  const bool ex = extra(cfg);
   if (dtype == ZF_F64)
-    stats_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(x), n, *cfg,
-                                                   partials, counts);
+    (ex ? stats_kernel<double, true> : stats_kernel<double, false>)<<<grid, kThreads, smem, s>>>(
+        static_cast<const double*>(x), n, *cfg, partials, counts);
   else if (dtype == ZF_F32)
-    stats_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(x), n, *cfg, partials,
-                                                  counts);
+    (ex ? stats_kernel<float, true> : stats_kernel<float, false>)<<<grid, kThreads, smem, s>>>(
+        static_cast<const float*>(x), n, *cfg, partials, counts);
   else
     return ZF_EDIST;
   return cuda_status(cudaGetLastError());

@@ -53,6 +53,13 @@ struct LaneCounts {
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
 };
 
+// mask |= bit if d is NaN (setp.nan on the fp64 pipe + a predicated add)
+__device__ __forceinline__ void or_if_nan(uint32_t& mask, double d, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %1, %1;\n\t@p or.b32 %0, %0, %2;\n\t}"
+      : "+r"(mask)
+      : "d"(d), "r"(bit));
+}
+
 template <typename OutT, bool VEC>
 struct StoreSink {
   using Out = OutT;
@@ -69,17 +76,40 @@ struct StoreSink {
     }
   }
   __device__ __forceinline__ void put(uint64_t k, OutT v, bool /*exc*/) { out[k] = v; }
+  __device__ __forceinline__ void flag(uint32_t& mask, double d, uint32_t bit) {
+    or_if_nan(mask, d, bit);
+  }
+};
+
+// Generate-and-aggregate (the reference's aggregate / bench loop): one running
+// fp64 sum per lane.  The NaN test that flags an exceptional sample also
+// predicates the add, so the fast path pays one DADD and no integer work.
+struct SumSink {
+  using Out = double;
+  static constexpr int V = 2;
+  double s = 0.0;
+  __device__ __forceinline__ void flag(uint32_t& mask, double d, uint32_t bit) {
+    asm("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %2, %2;\n\t@p or.b32 %0, %0, %3;"
+        "\n\t@!p add.rn.f64 %1, %1, %2;\n\t}"
+        : "+r"(mask), "+d"(s)
+        : "d"(d), "r"(bit));
+  }
+  __device__ __forceinline__ void put_vec(uint64_t, const double*, uint32_t) {}
+  __device__ __forceinline__ void put(uint64_t, double v, bool exc) {
+    if (!exc) s = __dadd_rn(s, v);
+  }
 };
 
 // Validation statistics: raw power sums x^1..x^5 (quality.py:92-106), an
 // equal-width histogram with under/overflow bins and threshold counts.
-struct StatsSink {
+template <bool EXTRA>  // false: moments only (no histogram / thresholds)
+struct StatsSinkT {
   using Out = double;
   static constexpr int V = 2;
   double s[5] = {0, 0, 0, 0, 0};
   unsigned long long thr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned int* hist;  // smem, nbins + 2
-  double lo, inv_w;
+  double lo, inv_w, tmin;  // tmin: smallest threshold (+inf if none)
   int nbins, nthresh;
   bool abs_t;
   const double* t;  // thresholds (smem)
@@ -94,12 +124,18 @@ struct StatsSink {
     s[3] += p;
     p *= x;
     s[4] += p;
-    const double a = abs_t ? fabs(x) : x;
-    for (int q = 0; q < nthresh; ++q) thr[q] += a > t[q];
-    if (nbins) {
-      const double f = (x - lo) * inv_w;
-      int b = f < 0.0 ? -1 : (f >= (double)nbins ? nbins : (int)f);
-      atomicAdd(hist + (b + 1), 1u);
+    if constexpr (EXTRA) {
+      const double a = abs_t ? fabs(x) : x;
+      if (a > tmin) {  // tail counts: almost every sample is below all thresholds
+#pragma unroll
+        for (int q = 0; q < 8; ++q)  // fixed trip count keeps thr[] in registers
+          if (q < nthresh) thr[q] += a > t[q];
+      }
+      if (nbins) {
+        const double f = (x - lo) * inv_w;
+        int b = f < 0.0 ? -1 : (f >= (double)nbins ? nbins : (int)f);
+        atomicAdd(hist + (b + 1), 1u);
+      }
     }
   }
   __device__ __forceinline__ void put_vec(uint64_t, const double* v, uint32_t exc_bits) {
@@ -110,14 +146,12 @@ struct StatsSink {
   __device__ __forceinline__ void put(uint64_t, double v, bool exc) {
     if (!exc) add(v);
   }
+  __device__ __forceinline__ void flag(uint32_t& mask, double d, uint32_t bit) {
+    or_if_nan(mask, d, bit);
+  }
 };
+using StatsSink = StatsSinkT<true>;
 
-// mask |= bit if d is NaN (setp.nan on the fp64 pipe + a predicated add)
-__device__ __forceinline__ void or_if_nan(uint32_t& mask, double d, uint32_t bit) {
-  asm("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %1, %1;\n\t@p or.b32 %0, %0, %2;\n\t}"
-      : "+r"(mask)
-      : "d"(d), "r"(bit));
-}
 
 // Pass 1 of one warp tile: samples [base, min(base + kTile, n)) of the counter
 // stream (seed, ctr_base).  Returns the lane's mask of exceptional samples
@@ -146,7 +180,7 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
         // fast value itself flags an exceptional sample: a DSETP on the fp64
         // pipe instead of integer compare/select work on the busy ALU pipe.
         const double d = fast_value<DIST>(sx, mix13(st + (uint64_t)e * kGamma));
-        or_if_nan(mask, d, 1u << (it * V + e));
+        sink.flag(mask, d, 1u << (it * V + e));
         v[e] = to_out<OutT>(d);
       }
       sink.put_vec(k_lane + (uint64_t)it * 32 * V, v, mask >> (it * V));

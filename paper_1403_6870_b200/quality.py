@@ -43,8 +43,12 @@ class StatsResult:
         return [s / self.n for s in self.sums]
 
 
-def _cfg(hist=None, thresholds=(), abs_thresh=False) -> _lib.StatsCfg:
+def _cfg(hist=None, thresholds=(), abs_thresh=False, moments=5) -> _lib.StatsCfg:
+    if not 1 <= moments <= 5:
+        raise ValueError("moments must be in 1..5")
     cfg = _lib.StatsCfg()
+    # 1 moment with no histogram / thresholds selects the sum-only kernel
+    cfg.moments = 1 if moments == 1 else 5
     if hist is not None:
         cfg.hist_lo, cfg.hist_hi, cfg.nbins = float(hist[0]), float(hist[1]), int(hist[2])
     if len(thresholds) > 8:
@@ -84,7 +88,7 @@ def device_sums(sampler, n: int, moments: int = 5, hist=None, thresholds=(), abs
     src = sampler.source
     if src.gid != _lib.GEN_CTR:
         raise ValueError("fused statistics need a production ('ctr') source")
-    cfg = _cfg(hist, thresholds, abs_thresh)
+    cfg = _cfg(hist, thresholds, abs_thresh, moments)
     partials, counts = _buffers(sampler.device, n, cfg)
     with torch.cuda.device(sampler.device):
         _lib.check(_lib.lib().zf_fill_stats(

@@ -12,6 +12,9 @@ c5   tail stress, one GPU's share of config 5: N(0,1) n = 2^33, seed 99, counts 
      |x| > 5, 6, 7 and Exp(1) n = 2^33 counts of x > X[1], vs analytic tail mass
      (5-sigma binomial); generate-and-count, nothing materialised
 f32  fp32 production fills (n = 2^28) for both distributions
+agg  generate-and-aggregate (the reference's bench loop):
+     sum of n = 2^32 draws with nothing written to HBM (sum-only kernel), and
+     the 5-moment validation kernel; kernel time by CUDA events
 """
 import json
 import math
@@ -120,6 +123,44 @@ def f32(n=1 << 28):
         sec = ev_time(lambda: s.fill(out))
         emit({"config": "f32", "dist": dist, "n": n, "samples_per_s": n / sec,
               "gbs": 4 * n / sec / 1e9})
+
+
+def agg(n=1 << 32):
+    import ctypes as C
+    from paper_1403_6870_b200 import _lib
+    for dist, cls in (("exp", zf.ExpSampler), ("normal", zf.NormalSampler)):
+        s = cls(source=zf.UniformSource.counter(1234), device=dev)
+        row = {"config": "agg", "dist": dist, "n": n}
+        for name, moments in (("sum", 1), ("moments5", 5)):
+            cfg = quality._cfg(moments=moments)
+            partials, counts = quality._buffers(dev, n, cfg)
+            lib = _lib.lib()
+
+            def run():
+                _lib.check(lib.zf_fill_stats(s._dev_tables.handle, s._dist, 1234, 0, n,
+                                             C.byref(cfg), partials.data_ptr(),
+                                             counts.data_ptr(), _lib.stream_handle(dev)))
+            sec = ev_time(run)
+            row[f"{name}_samples_per_s"] = n / sec
+        sec = wall(lambda: s.aggregate(n))
+        row["aggregate_call_samples_per_s"] = n / sec
+        emit(row)
+    # validation reductions of an existing 2^28 fp64 buffer (HBM read bound)
+    m = 1 << 28
+    buf = zf.NormalSampler(source=zf.UniformSource.counter(5), device=dev).fill(m)
+    row = {"config": "buffer_stats", "n": m}
+    for name, hist in (("moments5", None), ("moments5_hist1024", (-6.0, 6.0, 1024))):
+        cfg = quality._cfg(hist=hist)
+        partials, counts = quality._buffers(dev, m, cfg)
+        lib = _lib.lib()
+
+        def run():
+            _lib.check(lib.zf_stats(_lib.F64, buf.data_ptr(), m, C.byref(cfg),
+                                    partials.data_ptr(), counts.data_ptr(),
+                                    _lib.stream_handle(dev)))
+        sec = ev_time(run)
+        row[f"{name}_gbs"] = 8 * m / sec / 1e9
+    emit(row)
 
 
 if __name__ == "__main__":
