@@ -13,7 +13,9 @@
  * /root/reference/pkg/src/zigfast/):
  *
  *   zf_tables_create   _packs.exp_pack / normal_pack / make_alias      _packs.py:31-64
+ *   zf_trad_tables_create  traditional._pack (trad samplers)         traditional.py:113-135
  *   zf_fill            fill_exp / fill_normal (new counter generator)  _kernels.py:226-260, 597-689
+ *                      dist ZF_TRAD_*: fill_trad_exp / fill_trad_normal _kernels.py:982-1004, 1149-1176
  *   zf_fill_gid        fill_exp(state, gid, *pack, out) incl. gid 0/1/2  _kernels.py:226-228, 597-600
  *   zf_fill_replay     the same, gid 2 (replay) on a device word buffer _kernels.py:83-88
  *   zf_words           next_block(state, gid, out)                     _kernels.py:91-94
@@ -37,6 +39,10 @@ extern "C" {
 /* distributions */
 #define ZF_EXP 0    /* Exponential(1)                      */
 #define ZF_NORMAL 1 /* N(0,1) = half-normal magnitude + sign */
+/* traditional (Marsaglia-Tsang) ziggurat baseline, traditional.py:56-207,
+ * _kernels.py:933-1277; needs a handle from zf_trad_tables_create */
+#define ZF_TRAD_EXP 2
+#define ZF_TRAD_NORMAL 3
 
 /* output element types */
 #define ZF_F64 0
@@ -81,6 +87,20 @@ typedef struct zf_table_pack {
   double tailx; /* X[1] */
 } zf_table_pack;
 
+/* Traditional-ziggurat pack: the tuple traditional._pack returns
+ * (traditional.py:113-121).  i_max = 256 entries each: se = edge * 2^-64
+ * (exp) / 2^-63 (normal), kk = integer fast-accept thresholds
+ * (_int_thresholds, traditional.py:99-110), flo/fh = wedge strip [f_{i-1},
+ * f_i] (slot 0 unused), r = base abscissa (tail start). */
+typedef struct zf_trad_pack {
+  int64_t i_max;
+  const double* se;
+  const uint64_t* kk;
+  const double* flo;
+  const double* fh;
+  double r;
+} zf_trad_pack;
+
 /* Per-sample path record (oracle mode). */
 typedef struct zf_path_rec {
   uint64_t start;    /* logical word offset of the draw's first word */
@@ -122,6 +142,10 @@ const char* zf_strerror(int status);
  * for its tail).  Either pointer may describe the reference default tables. */
 int zf_tables_create(const zf_table_pack* exp_pack, const zf_table_pack* halfnormal_pack,
                      int device, zf_tables** out);
+/* Traditional-ziggurat handle (dists ZF_TRAD_EXP / ZF_TRAD_NORMAL only):
+ * replaces the per-sampler `_pack` of _TraditionalSampler (traditional.py:124-135). */
+int zf_trad_tables_create(const zf_trad_pack* exp_pack, const zf_trad_pack* hn_pack, int device,
+                          zf_tables** out);
 int zf_tables_destroy(zf_tables* t);
 
 /* Production mode: sample k (0 <= k < n) of the call is global sample

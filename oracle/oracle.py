@@ -26,7 +26,7 @@ LIB_PATH = HERE / "_build" / "libzf_oracle.so"
 DATA = HERE.parent / "paper_1403_6870_b200" / "data"
 
 SRC_XOSHIRO, SRC_SPLITMIX, SRC_REPLAY, SRC_CTR = 0, 1, 2, 3
-EXP, NORMAL = 0, 1
+EXP, NORMAL, TRAD_EXP, TRAD_NORMAL = 0, 1, 2, 3
 
 REC_DTYPE = np.dtype([("start", "<u8"), ("nwords", "<u4"), ("layer", "u1"),
                       ("path", "u1"), ("attempts", "<u2")])
@@ -66,6 +66,12 @@ def lib():
         L.orc_fill_sharded.restype = C.c_int
         L.orc_fill_sharded.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                        C.c_uint64, C.c_int]
+        dp = C.POINTER(C.c_double)
+        L.orc_trad_solve.restype = C.c_int
+        L.orc_trad_solve.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp]
+        L.orc_trad_pack_arrays.restype = None
+        L.orc_trad_pack_arrays.argtypes = [C.c_int, C.c_int, dp, dp, dp, C.c_double, C.c_double,
+                                           dp, u64p, dp, dp]
         _lib = L
     return _lib
 
@@ -130,18 +136,55 @@ class OraclePack:
                       _ptr(self.prob).value, _ptr(self.alias).value, float(t["x"][1]))
 
 
+class TradPack(C.Structure):
+    _fields_ = [("i_max", C.c_int64), ("se", C.c_void_p), ("kk", C.c_void_p),
+                ("flo", C.c_void_p), ("fh", C.c_void_p), ("r", C.c_double)]
+
+
+class OracleTradPack:
+    """Traditional tables solved by the C restatement of solve_traditional
+    (traditional.py:56-96) and packed like traditional._pack (:113-121)."""
+
+    def __init__(self, kind: str, i_max: int = 256):
+        code = 0 if kind == "exponential" else 1
+        dp = C.POINTER(C.c_double)
+        self.x, self.f, self.k = (np.empty(i_max) for _ in range(3))
+        r, v = C.c_double(), C.c_double()
+        rc = lib().orc_trad_solve(code, i_max, self.x.ctypes.data_as(dp),
+                                  self.f.ctypes.data_as(dp), self.k.ctypes.data_as(dp),
+                                  C.byref(r), C.byref(v))
+        assert rc == 0, rc
+        self.r, self.v = r.value, v.value
+        self.se, self.flo, self.fh = (np.empty(i_max) for _ in range(3))
+        self.kk = np.empty(i_max, dtype=np.uint64)
+        lib().orc_trad_pack_arrays(code, i_max, self.x.ctypes.data_as(dp),
+                                   self.f.ctypes.data_as(dp), self.k.ctypes.data_as(dp),
+                                   self.r, self.v, self.se.ctypes.data_as(dp), _u64p(self.kk),
+                                   self.flo.ctypes.data_as(dp), self.fh.ctypes.data_as(dp))
+        self.c = TradPack(i_max, _ptr(self.se).value, _ptr(self.kk).value, _ptr(self.flo).value,
+                          _ptr(self.fh).value, self.r)
+
+
 _packs = {}
 
 
-def packs():
-    if not _packs:
+def packs(dist=EXP):
+    """(h, e) pack pair for a distribution code (modified or traditional)."""
+    if _dist(dist) in (TRAD_EXP, TRAD_NORMAL):
+        if "texp" not in _packs:
+            _packs["texp"] = OracleTradPack("exponential")
+            _packs["thn"] = OracleTradPack("halfnormal")
+        return _packs["thn"], _packs["texp"]
+    if "exp" not in _packs:
         _packs["exp"] = OraclePack("exponential")
         _packs["hn"] = OraclePack("halfnormal")
     return _packs["hn"], _packs["exp"]
 
 
 def _dist(dist) -> int:
-    return {"exp": EXP, "exponential": EXP, "normal": NORMAL, EXP: EXP, NORMAL: NORMAL}[dist]
+    return {"exp": EXP, "exponential": EXP, "normal": NORMAL, "trad_exp": TRAD_EXP,
+            "trad_normal": TRAD_NORMAL, EXP: EXP, NORMAL: NORMAL, TRAD_EXP: TRAD_EXP,
+            TRAD_NORMAL: TRAD_NORMAL}[dist]
 
 
 # --- word streams -------------------------------------------------------------
@@ -171,7 +214,7 @@ def derive_seed(base: int, stream: int) -> int:
 def fill_stream(dist, n: int, *, generator="xoshiro256++", seed=0, replay_words=None,
                 cursor=0, records=False):
     """Reference fill over a sequential stream; returns (values, counters, recs, used)."""
-    h, e = packs()
+    h, e = packs(dist)
     out = np.empty(n, dtype=np.float64)
     cnt = np.zeros(6, dtype=np.int64)
     recs = np.zeros(n, dtype=REC_DTYPE) if records else None
@@ -192,7 +235,7 @@ def fill_stream(dist, n: int, *, generator="xoshiro256++", seed=0, replay_words=
 
 def fill_ctr(dist, n: int, seed: int, ctr_base: int = 0, records=False):
     """Production ("ctr") stream restated on the CPU; returns (values, counters, recs)."""
-    h, e = packs()
+    h, e = packs(dist)
     out = np.empty(n, dtype=np.float64)
     cnt = np.zeros(6, dtype=np.int64)
     recs = np.zeros(n, dtype=REC_DTYPE) if records else None
@@ -208,7 +251,7 @@ def ctr_words(seed: int, K: int, m: int) -> np.ndarray:
 
 
 def aggregate(dist, n: int, seed: int) -> float:
-    h, e = packs()
+    h, e = packs(dist)
     st = xoshiro_state(seed)
     return float(lib().orc_aggregate(_dist(dist), C.byref(h.c), C.byref(e.c), SRC_XOSHIRO,
                                      _u64p(st), n))
@@ -217,7 +260,7 @@ def aggregate(dist, n: int, seed: int) -> float:
 def fill_sharded(dist, n: int, seed: int, threads: int | None = None,
                  out: np.ndarray | None = None) -> np.ndarray:
     """The reference's --jobs sharding (quality.py:121-126) on `threads` host threads."""
-    h, e = packs()
+    h, e = packs(dist)
     threads = threads or len(os.sched_getaffinity(0))
     out = np.empty(n, dtype=np.float64) if out is None else out
     rc = lib().orc_fill_sharded(_dist(dist), C.byref(h.c), C.byref(e.c), seed & (2**64 - 1),

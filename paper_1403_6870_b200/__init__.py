@@ -15,12 +15,14 @@ from __future__ import annotations
 import threading
 
 from .errors import (BitBudgetExceeded, DeviceError, EmptyWeights, ExtensionMissing,
-                     FormatError, ZigfastError)
+                     FormatError, NonConvergence, ZigfastError)
 from .batch import BatchPlan, fill_batch
 from .quality import EXPECTED_MOMENTS, QualityReport, run_quality
 from .samplers import ExpSampler, NormalSampler, PathCounts
 from .tables import (EXPONENTIAL, HALF_NORMAL, AliasTable, ZigguratTables, build_alias,
                      default_tables, load, save)
+from .traditional import (TraditionalExpSampler, TraditionalNormalSampler, TraditionalTables,
+                          solve_traditional)
 from .uniform import UniformSource, auto_seed_value, derive_seed, split_index
 
 __version__ = "0.1.0"
@@ -59,8 +61,10 @@ def normal(size: int, device=None):
 __all__ = [
     "AliasTable", "BatchPlan", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
     "EmptyWeights", "ExpSampler", "ExtensionMissing", "FormatError", "HALF_NORMAL",
-    "NormalSampler", "PathCounts", "QualityReport", "UniformSource", "ZigfastError",
+    "NonConvergence", "NormalSampler", "PathCounts", "QualityReport",
+    "TraditionalExpSampler", "TraditionalNormalSampler", "TraditionalTables", "UniformSource",
+    "ZigfastError",
     "ZigguratTables", "auto_seed_value", "build_alias", "default_tables", "derive_seed",
     "exponential", "fill_batch", "load", "normal", "run_quality", "save", "seed",
-    "split_index", "__version__",
+    "solve_traditional", "split_index", "__version__",
 ]

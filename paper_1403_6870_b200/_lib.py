@@ -29,8 +29,9 @@ PATH_FAST, PATH_TAIL, PATH_BOXFAST, PATH_BOXEVAL = 1, 2, 4, 8
 EXPORTS = (
     "zf_abi_version", "zf_strerror", "zf_tables_create", "zf_tables_destroy", "zf_fill",
     "zf_fill_stats", "zf_stats", "zf_stats_blocks", "zf_fill_replay", "zf_fill_gid", "zf_words",
-    "zf_xoshiro_jump", "zf_xoshiro_pow2_poly", "zf_fill_batch",
+    "zf_xoshiro_jump", "zf_xoshiro_pow2_poly", "zf_fill_batch", "zf_trad_tables_create",
 )
+EXP, NORMAL, TRAD_EXP, TRAD_NORMAL = 0, 1, 2, 3
 
 REC_DTYPE = np.dtype([("start", "<u8"), ("nwords", "<u4"), ("layer", "u1"),
                       ("path", "u1"), ("attempts", "<u2")])
@@ -41,6 +42,11 @@ class TablePack(C.Structure):
                 ("xlo", C.c_void_p), ("xw", C.c_void_p), ("flo", C.c_void_p),
                 ("fh", C.c_void_p), ("eps", C.c_double), ("prob", C.c_void_p),
                 ("alias", C.c_void_p), ("tailx", C.c_double)]
+
+
+class TradPack(C.Structure):
+    _fields_ = [("i_max", C.c_int64), ("se", C.c_void_p), ("kk", C.c_void_p),
+                ("flo", C.c_void_p), ("fh", C.c_void_p), ("r", C.c_double)]
 
 
 class Request(C.Structure):
@@ -89,6 +95,8 @@ def lib():
                 "zf_xoshiro_jump": (i32, [u64p, u64]),
                 "zf_xoshiro_pow2_poly": (i32, [i32, u64p]),
                 "zf_fill_batch": (i32, [vp, C.POINTER(Request), i32, i32, vp, vp]),
+                "zf_trad_tables_create": (i32, [C.POINTER(TradPack), C.POINTER(TradPack), i32,
+                                                C.POINTER(vp)]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -144,6 +152,26 @@ class DeviceTables:
             pass
 
 
+class DeviceTradTables(DeviceTables):
+    """The uploaded traditional packs (exp + half-normal) on one device."""
+
+    def __init__(self, exp_pack, hn_pack, device_index: int):
+        self._keep = []
+        packs = [self._tpack(exp_pack), self._tpack(hn_pack)]
+        handle = C.c_void_p()
+        check(lib().zf_trad_tables_create(C.byref(packs[0]), C.byref(packs[1]), device_index,
+                                          C.byref(handle)))
+        self.handle = handle
+        self.device_index = device_index
+
+    def _tpack(self, p) -> TradPack:
+        se, flo, fh = (np.ascontiguousarray(a, dtype=np.float64) for a in (p.se, p.flo, p.fh))
+        kk = np.ascontiguousarray(p.kk, dtype=np.uint64)
+        self._keep.extend((se, flo, fh, kk))
+        return TradPack(se.size, se.ctypes.data, kk.ctypes.data, flo.ctypes.data,
+                        fh.ctypes.data, p.r)
+
+
 _tables_cache: dict = {}
 
 
@@ -154,6 +182,18 @@ def device_tables(exp_tables, hn_tables, device_index: int) -> DeviceTables:
     hit = _tables_cache.get(key)
     if hit is None or hit[0] is not exp_tables or hit[1] is not hn_tables:
         dt = DeviceTables(make_pack(exp_tables), make_pack(hn_tables), device_index)
+        hit = (exp_tables, hn_tables, dt)
+        _tables_cache[key] = hit
+    return hit[2]
+
+
+def device_trad_tables(exp_tables, hn_tables, device_index: int) -> DeviceTradTables:
+    """Cached upload of a traditional (exp, half-normal) table pair."""
+    from .traditional import trad_pack
+    key = ("trad", id(exp_tables), id(hn_tables), device_index)
+    hit = _tables_cache.get(key)
+    if hit is None or hit[0] is not exp_tables or hit[1] is not hn_tables:
+        dt = DeviceTradTables(trad_pack(exp_tables), trad_pack(hn_tables), device_index)
         hit = (exp_tables, hn_tables, dt)
         _tables_cache[key] = hit
     return hit[2]

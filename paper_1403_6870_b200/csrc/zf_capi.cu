@@ -49,6 +49,62 @@ void fill_devpack(const zf_table_pack* p, DevPack* d) {
   for (int i = n; i < (int)(sizeof d->sx / sizeof d->sx[0]); ++i) d->sx[i] = NAN;
 }
 
+int check_trad_pack(const zf_trad_pack* p) {
+  if (!p || !p->se || !p->kk || !p->flo || !p->fh) return ZF_EINVAL;
+  // the kernels index by the low byte of the word (_kernels.py: i = u & MASK8)
+  if (p->i_max != kSlots || !(p->r > 0.0)) return ZF_ETABLE;
+  return ZF_OK;
+}
+
+// traditional pack in the DevPack layout (see zf_device.cuh)
+void fill_trad_devpack(const zf_trad_pack* p, DevPack* d) {
+  std::memset(d, 0, sizeof *d);
+  for (int i = 0; i < kSlots; ++i) {
+    d->sx[i + 1] = p->se[i];
+    d->kk[i] = p->kk[i];
+    d->flo[i] = p->flo[i];
+    d->fh[i] = p->fh[i];
+  }
+  d->tailx = p->r;
+  d->lmax = kSlots;
+  d->nslots = kSlots;
+}
+
+// device checks, pool policy and the upload shared by both table kinds
+int upload_tables(zf_tables* t, int device) {
+  int ndev = 0;
+  ZF_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return ZF_EDEVICE;
+  cudaDeviceProp prop;
+  ZF_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return ZF_EDEVICE;  // sm_100a cubin only
+  t->device = device;
+  t->sm_count = prop.multiProcessorCount;
+  t->dev = nullptr;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) {
+    // Oracle-mode scratch comes from the device's stream-ordered pool; keep
+    // freed blocks cached instead of returning them to the driver at every
+    // synchronisation (re-mapping ~1 GB per fill otherwise dominates).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    e = cudaMalloc(&t->dev, sizeof(DevTables));
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(t->dev, &t->host, sizeof(DevTables), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (t->dev) cudaFree(t->dev);
+    t->dev = nullptr;
+    return (int)e;
+  }
+  return ZF_OK;
+}
+
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
@@ -79,38 +135,35 @@ int zf_tables_create(const zf_table_pack* exp_pack, const zf_table_pack* hn_pack
   ZF_TRY_STATUS(check_pack(exp_pack));
   ZF_TRY_STATUS(check_pack(hn_pack));
   if (exp_pack->eps < 0.0) return ZF_ETABLE;
-  int ndev = 0;
-  ZF_TRY(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return ZF_EDEVICE;
-  cudaDeviceProp prop;
-  ZF_TRY(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10) return ZF_EDEVICE;  // sm_100a cubin only
   zf_tables* t = new (std::nothrow) zf_tables;
   if (!t) return ZF_EINVAL;
-  t->device = device;
-  t->sm_count = prop.multiProcessorCount;
+  t->kind = kKindModified;
   fill_devpack(exp_pack, &t->host.ex);
   fill_devpack(hn_pack, &t->host.hn);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) {
-    // Oracle-mode scratch comes from the device's stream-ordered pool; keep
-    // freed blocks cached instead of returning them to the driver at every
-    // synchronisation (re-mapping ~1 GB per fill otherwise dominates).
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    e = cudaMalloc(&t->dev, sizeof(DevTables));
-  }
-  if (e == cudaSuccess) e = cudaMemcpy(t->dev, &t->host, sizeof(DevTables), cudaMemcpyHostToDevice);
-  cudaSetDevice(prev);
-  if (e != cudaSuccess) {
-    if (t->dev) cudaFree(t->dev);
+  const int rc = upload_tables(t, device);
+  if (rc != ZF_OK) {
     delete t;
-    return (int)e;
+    return rc;
+  }
+  *out = t;
+  return ZF_OK;
+}
+
+int zf_trad_tables_create(const zf_trad_pack* exp_pack, const zf_trad_pack* hn_pack, int device,
+                          zf_tables** out) {
+  if (!out) return ZF_EINVAL;
+  *out = nullptr;
+  ZF_TRY_STATUS(check_trad_pack(exp_pack));
+  ZF_TRY_STATUS(check_trad_pack(hn_pack));
+  zf_tables* t = new (std::nothrow) zf_tables;
+  if (!t) return ZF_EINVAL;
+  t->kind = kKindTraditional;
+  fill_trad_devpack(exp_pack, &t->host.ex);
+  fill_trad_devpack(hn_pack, &t->host.hn);
+  const int rc = upload_tables(t, device);
+  if (rc != ZF_OK) {
+    delete t;
+    return rc;
   }
   *out = t;
   return ZF_OK;

@@ -38,9 +38,17 @@ __host__ __device__ __forceinline__ uint64_t mix13(uint64_t z) {
 // every byte i: the fast loop reads it branch-free, and entries past L_max hold
 // NaN so an exceptional byte yields a NaN fast value (its detection flag).
 // Doubles first so every array is 16-byte aligned.
+//
+// The traditional ziggurat (traditional.py:113-121 `_pack`) reuses the layout:
+// sx[i+1] = edge[i]*2^-64 (exp) / *2^-63 (normal), kk[] (aliasing xlo) = the
+// integer fast-accept thresholds, flo/fh = the wedge strip, tailx = r,
+// lmax = nslots = 256; the other arrays are unused.
 struct alignas(16) DevPack {
   double sx[kSlots + 2];
-  double xlo[kSlots];
+  union {
+    double xlo[kSlots];
+    uint64_t kk[kSlots];
+  };
   double xw[kSlots];
   double flo[kSlots];
   double fh[kSlots];
@@ -62,8 +70,105 @@ struct alignas(16) DevTables {
 
 static_assert(sizeof(DevPack) % 16 == 0, "DevPack must be int4-copyable");
 
+// Distribution traits.  A table handle holds either the modified packs
+// (hn = half-normal, ex = exponential) or the traditional ones in the same
+// two slots; normal kernels of the modified algorithm also stage `ex` for the
+// Marsaglia tail.
+template <int DIST>
+constexpr bool kTrad = DIST == ZF_TRAD_EXP || DIST == ZF_TRAD_NORMAL;
+template <int DIST>
+constexpr bool kSigned = DIST == ZF_NORMAL || DIST == ZF_TRAD_NORMAL;
+template <int DIST>
+constexpr int kPacksOf = DIST == ZF_NORMAL ? 2 : 1;
+template <int DIST>
+__host__ __device__ __forceinline__ const DevPack* primary_pack(const DevTables* t) {
+  return kSigned<DIST> ? &t->hn : &t->ex;
+}
+
 __device__ __forceinline__ double u01(uint64_t u) {
   return __dmul_rn(__ull2double_rn(u), 0x1p-64);
+}
+
+// (float64(u) + 1.0) * 2^-64 in (0, 1] (_u01_pos, _kernels.py:103-105)
+__device__ __forceinline__ double u01_pos(uint64_t u) {
+  return __dmul_rn(__dadd_rn(__ull2double_rn(u), 1.0), 0x1p-64);
+}
+
+// ---------------------------------------------------------------------------
+// correctly rounded natural log (the traditional sampler returns log values,
+// _kernels.py:945,1103, so its tail samples need the libm result, not CUDA's
+// 1-ulp log).  Double-double evaluation, relative error ~2^-100, then one
+// rounding: equals the correctly rounded log except when the exact value lies
+// within ~2^-100 of a rounding boundary.  Rare path (tails only).
+// ---------------------------------------------------------------------------
+
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ DD quick_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ DD two_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  const DD t = two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  DD p = two_prod(a.hi, b.hi);
+  p.lo = __fma_rn(a.hi, b.lo, p.lo);
+  p.lo = __fma_rn(a.lo, b.hi, p.lo);
+  return quick_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ DD dd_div(DD a, DD b) {
+  const double q1 = __ddiv_rn(a.hi, b.hi);
+  DD r = dd_add(a, dd_mul(b, DD{-q1, 0.0}));
+  const double q2 = __ddiv_rn(r.hi, b.hi);
+  r = dd_add(r, dd_mul(b, DD{-q2, 0.0}));
+  const double q3 = __ddiv_rn(r.hi, b.hi);
+  return dd_add(quick_two_sum(q1, q2), DD{q3, 0.0});
+}
+
+// log(x) for finite x > 0 (normal or subnormal), correctly rounded as above.
+static __device__ __noinline__ double log_cr(double x) {
+  int e = 0;
+  double m = frexp(x, &e);  // x = m * 2^e, m in [0.5, 1)
+  if (m < 0.70710678118654752) {
+    m = __dmul_rn(m, 2.0);
+    --e;
+  }  // m in [sqrt(1/2), sqrt(2))
+  // log(m) = 2 atanh(t), t = (m - 1) / (m + 1); |t| <= 0.1716
+  const DD num = DD{__dsub_rn(m, 1.0), 0.0};  // exact (Sterbenz)
+  const DD den = two_sum(m, 1.0);
+  const DD t = dd_div(num, den);
+  const DD t2 = dd_mul(t, t);
+  // sum_{k>=0} t^(2k) / (2k+1), k < 24 (t^48 < 2^-120)
+  DD acc = DD{1.0 / 47.0, 0.0};
+  for (int k = 22; k >= 0; --k) {
+    const double d = (double)(2 * k + 1);
+    const double ch = __ddiv_rn(1.0, d);
+    const DD c = DD{ch, __ddiv_rn(-__fma_rn(ch, d, -1.0), d)};  // 1/d to ~2^-106
+    acc = dd_add(c, dd_mul(acc, t2));
+  }
+  DD lm = dd_mul(dd_mul(DD{2.0, 0.0}, t), acc);
+  constexpr double kLn2Hi = 0x1.62e42fefa39efp-1;
+  constexpr double kLn2Lo = 0x1.abc9e3b39803fp-56;
+  const DD el = dd_mul(DD{(double)e, 0.0}, DD{kLn2Hi, kLn2Lo});
+  const DD r = dd_add(el, lm);
+  return __dadd_rn(r.hi, r.lo);
 }
 
 // ---------------------------------------------------------------------------
@@ -254,21 +359,120 @@ __device__ double normal_draw(const DevPack& h, const DevPack& e, uint64_t u, S&
   return sg < 0 ? -val : val;
 }
 
+// ---------------------------------------------------------------------------
+// traditional ziggurat (trad_exp_one_counted / trad_normal_one_counted,
+// _kernels.py:956-979, :1117-1146): x = word * edge unconditionally, integer
+// fast accept, tail fallback in strip 0, otherwise one wedge test; any
+// rejection restarts with a fresh byte word.  Counter slots as the reference:
+// 0 byte words, 1 fast accepts, 2 wedge tests, 3 tail entries.
+// ---------------------------------------------------------------------------
+
+template <int DIST>
+__device__ __forceinline__ bool trad_fast(const uint64_t* kk, uint64_t u) {
+  const uint64_t a = (DIST == ZF_TRAD_NORMAL && (long long)u < 0) ? 0ull - u : u;
+  return a < kk[u & 0xFF];
+}
+
+template <class S, class C>
+__device__ double trad_exp_draw(const DevPack& p, uint64_t u, S& s, C& c) {
+  for (;;) {
+    c.add(0);
+    const int i = (int)(u & 0xFF);
+    const double x = __dmul_rn(__ull2double_rn(u), p.sx[i + 1]);
+    if (u < p.kk[i]) {
+      c.add(1);
+      c.path |= ZF_PATH_FAST;
+      return x;
+    }
+    if (i == 0) {
+      c.add(3);
+      c.path |= ZF_PATH_TAIL;
+      const double l = log_cr(u01_pos(s.next()));
+      if (S::kBounded && s.dead()) return 0.0;
+      return __dsub_rn(p.tailx, l);
+    }
+    c.add(2);
+    if (C::kOn) c.attempts++;
+    const double y = __dadd_rn(p.flo[i], __dmul_rn(u01(s.next()), p.fh[i]));
+    if (S::kBounded && s.dead()) return 0.0;
+    if (less_than_exp(y, -x)) {
+      c.path |= ZF_PATH_BOXEVAL;
+      return x;
+    }
+    u = s.next();
+    if (S::kBounded && s.dead()) return 0.0;
+  }
+}
+
+template <class S, class C>
+__device__ double trad_normal_draw(const DevPack& p, uint64_t u, S& s, C& c) {
+  for (;;) {
+    c.add(0);
+    const int i = (int)(u & 0xFF);
+    const long long sg = (long long)u;
+    const double x = __dmul_rn(__ll2double_rn(sg), p.sx[i + 1]);
+    if (trad_fast<ZF_TRAD_NORMAL>(p.kk, u)) {
+      c.add(1);
+      c.path |= ZF_PATH_FAST;
+      return x;
+    }
+    if (i == 0) {
+      c.add(3);
+      c.path |= ZF_PATH_TAIL;
+      for (;;) {
+        if (C::kOn) c.attempts++;
+        const double xt = __ddiv_rn(-log_cr(u01_pos(s.next())), p.tailx);
+        const double yt = -log_cr(u01_pos(s.next()));
+        if (S::kBounded && s.dead()) return 0.0;
+        if (__dadd_rn(yt, yt) > __dmul_rn(xt, xt)) {
+          const double v = __dadd_rn(p.tailx, xt);
+          return sg < 0 ? -v : v;
+        }
+      }
+    }
+    c.add(2);
+    if (C::kOn) c.attempts++;
+    const double y = __dadd_rn(p.flo[i], __dmul_rn(u01(s.next()), p.fh[i]));
+    if (S::kBounded && s.dead()) return 0.0;
+    if (less_than_exp(y, __dmul_rn(__dmul_rn(-0.5, x), x))) {
+      c.path |= ZF_PATH_BOXEVAL;
+      return x;
+    }
+    u = s.next();
+    if (S::kBounded && s.dead()) return 0.0;
+  }
+}
+
 template <int DIST, class S, class C>
 __device__ __forceinline__ double draw(const DevPack& prim, const DevPack& ex, uint64_t u, S& s,
                                        C& c) {
   if constexpr (DIST == ZF_EXP) {
     return exp_draw(prim, u, s, c);
-  } else {
+  } else if constexpr (DIST == ZF_NORMAL) {
     return normal_draw(prim, ex, u, s, c);
+  } else if constexpr (DIST == ZF_TRAD_EXP) {
+    return trad_exp_draw(prim, u, s, c);
+  } else {
+    return trad_normal_draw(prim, u, s, c);
   }
 }
 
-// Fast-path value of a first word (valid only when (u & 0xFF) < lmax).
+// Is a first word exceptional (anything but the one-word fast path)?
+template <int DIST>
+__device__ __forceinline__ bool exc_word(const DevPack& p, uint64_t u) {
+  if constexpr (kTrad<DIST>) {
+    return !trad_fast<DIST>(p.kk, u);
+  } else {
+    return ((uint32_t)u & 0xFFu) >= (uint32_t)p.lmax;
+  }
+}
+
+// Fast-path value of a first word (valid only when !exc_word; for the modified
+// algorithm it is NaN for every exceptional byte by the sx sentinel).
 template <int DIST>
 __device__ __forceinline__ double fast_value(const double* sx, uint64_t u) {
   const int i = (int)(u & 0xFF);
-  if constexpr (DIST == ZF_EXP) {
+  if constexpr (!kSigned<DIST>) {
     return __dmul_rn(__ull2double_rn(u), sx[i + 1]);
   } else {
     return __dmul_rn(__ll2double_rn((long long)u), sx[i + 1]);

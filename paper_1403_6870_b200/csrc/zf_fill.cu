@@ -40,10 +40,9 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
     fill_ctr_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
                     OutT* __restrict__ out, uint64_t n, unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  constexpr int kPacks = kPacksOf<DIST>;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
-  stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
-              kPacks * (int)sizeof(DevPack));
+  stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   const int lane = threadIdx.x & 31;
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kPacks * sizeof(DevPack)) +
                     (threadIdx.x >> 5) * kQueueCap;
@@ -140,9 +139,9 @@ static int pass2_override() {
 template <int DIST, typename OutT, bool COUNTED, bool VEC>
 static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, OutT* out,
                         uint64_t n, unsigned long long* counters, cudaStream_t s) {
-  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  constexpr int kPacks = kPacksOf<DIST>;
   auto kernel = fill_ctr_kernel<DIST, OutT, COUNTED, VEC, default_pass2<DIST, COUNTED>()>;
-  if (!COUNTED) {
+  if constexpr (!COUNTED && !kTrad<DIST>) {
     const int p2 = pass2_override();
     if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
     if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
@@ -169,6 +168,7 @@ static int launch_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base, voi
 
 int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,
                 void* out, uint64_t n, int64_t* counters, cudaStream_t s) {
+  ZF_TRY_STATUS(check_kind(t, dist));
   if (n == 0) return ZF_OK;
   if (dist == ZF_EXP && dtype == ZF_F64)
     return launch_dist<ZF_EXP, double>(t, seed, ctr_base, out, n, counters, s);
@@ -178,6 +178,14 @@ int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t
     return launch_dist<ZF_NORMAL, double>(t, seed, ctr_base, out, n, counters, s);
   if (dist == ZF_NORMAL && dtype == ZF_F32)
     return launch_dist<ZF_NORMAL, float>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F64)
+    return launch_dist<ZF_TRAD_EXP, double>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F32)
+    return launch_dist<ZF_TRAD_EXP, float>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F64)
+    return launch_dist<ZF_TRAD_NORMAL, double>(t, seed, ctr_base, out, n, counters, s);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F32)
+    return launch_dist<ZF_TRAD_NORMAL, float>(t, seed, ctr_base, out, n, counters, s);
   return ZF_EDIST;
 }
 
@@ -195,6 +203,7 @@ static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq, int nr
 int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
                       cudaStream_t s) {
   if (nreq <= 0) return nreq == 0 ? ZF_OK : ZF_EINVAL;
+  if (t->kind != kKindModified) return ZF_ETABLE;
   if (dtype != ZF_F64 && dtype != ZF_F32) return ZF_EDIST;
   const size_t esz = dtype == ZF_F64 ? 8 : 4;
   // every request must keep 16-byte alignment for the vector path

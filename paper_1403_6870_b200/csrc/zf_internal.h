@@ -7,6 +7,7 @@
 #include "zf_device.cuh"
 
 struct zf_tables {
+  int kind;  // zf::kKindModified or zf::kKindTraditional
   int device;
   int sm_count;
   zf::DevTables* dev;  // device copy: half-normal pack then exponential pack
@@ -29,6 +30,16 @@ inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? ZF_OK : (int)e
   } while (0)
 
 constexpr uint64_t kMaxCtr = 1ull << 44;  // primary counter range (see zf_device.cuh)
+
+constexpr int kKindModified = 0;
+constexpr int kKindTraditional = 1;
+// a dist code must match the algorithm of the handle's packs
+inline int check_kind(const zf_tables* t, int dist) {
+  if (dist != ZF_EXP && dist != ZF_NORMAL && dist != ZF_TRAD_EXP && dist != ZF_TRAD_NORMAL)
+    return ZF_EDIST;
+  const bool trad = dist == ZF_TRAD_EXP || dist == ZF_TRAD_NORMAL;
+  return trad == (t->kind == kKindTraditional) ? ZF_OK : ZF_ETABLE;
+}
 
 // launchers (zf_fill.cu)
 int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,

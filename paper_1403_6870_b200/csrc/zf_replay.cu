@@ -109,29 +109,32 @@ __global__ void scan_single(const T* __restrict__ in, T* __restrict__ out, uint6
 }
 
 // ---- A: classify / compact ---------------------------------------------------
-__global__ void rp_count_exc(Window win, uint32_t lmax, uint32_t* __restrict__ bcnt) {
+template <int DIST>
+__global__ void rp_count_exc(Window win, const DevPack* __restrict__ P,
+                             uint32_t* __restrict__ bcnt) {
   __shared__ uint32_t wb[32];
   const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
   uint32_t c = 0;
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
     const uint64_t p = p0 + j;
-    if (p < win.L) c += ((uint32_t)win.word(p) & 0xFFu) >= lmax;
+    if (p < win.L) c += exc_word<DIST>(*P, win.word(p));
   }
   uint32_t tot;
   block_exclusive<uint32_t>(c, 0u, Add(), wb, &tot);
   if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
 }
 
-__global__ void rp_compact_exc(Window win, uint32_t lmax, const uint32_t* __restrict__ boff,
-                               uint32_t* __restrict__ E) {
+template <int DIST>
+__global__ void rp_compact_exc(Window win, const DevPack* __restrict__ P,
+                               const uint32_t* __restrict__ boff, uint32_t* __restrict__ E) {
   __shared__ uint32_t wb[32];
   const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
   uint32_t flags = 0, c = 0;
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
     const uint64_t p = p0 + j;
-    const uint32_t f = p < win.L && ((uint32_t)win.word(p) & 0xFFu) >= lmax;
+    const uint32_t f = p < win.L && exc_word<DIST>(*P, win.word(p));
     flags |= f << j;
     c += f;
   }
@@ -154,10 +157,9 @@ __global__ void __launch_bounds__(kRT)
     rp_draw_exc(const DevTables* __restrict__ gt, Window win, const uint32_t* __restrict__ E,
                 uint32_t m, ExcOut o) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  constexpr int kPacks = kPacksOf<DIST>;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
-  stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
-              kPacks * (int)sizeof(DevPack));
+  stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   __syncthreads();
   const uint32_t i = blockIdx.x * kRT + threadIdx.x;
   if (i >= m) return;
@@ -269,12 +271,9 @@ __global__ void __launch_bounds__(kRT)
     rp_emit(const DevTables* __restrict__ gt, Window win, EmitArgs a, OutT* __restrict__ out) {
   __shared__ uint32_t wb[32];
   __shared__ double sx[kSlots + 2];
-  __shared__ int lmax_s;
-  const DevPack* P = DIST == ZF_NORMAL ? &gt->hn : &gt->ex;
+  const DevPack* P = primary_pack<DIST>(gt);
   for (int i = threadIdx.x; i < kSlots + 2; i += blockDim.x) sx[i] = P->sx[i];
-  if (threadIdx.x == 0) lmax_s = P->lmax;
   __syncthreads();
-  const uint32_t lmax = (uint32_t)lmax_s;
   const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
   uint32_t ex_flags = 0, st_flags = 0, ce = 0, cs = 0;
   uint64_t wds[kRI];
@@ -284,7 +283,7 @@ __global__ void __launch_bounds__(kRT)
     wds[j] = 0;
     if (p < win.L) {
       wds[j] = win.word(p);
-      const uint32_t e = ((uint32_t)wds[j] & 0xFFu) >= lmax;
+      const uint32_t e = exc_word<DIST>(*P, wds[j]);
       const uint32_t s = a.interior[p] == 0;
       ex_flags |= e << j;
       st_flags |= s << j;
@@ -445,8 +444,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   if (debug_on()) fprintf(stderr, "[zf] replay_window L=%llu nwords=%llu cursor=%llu n=%llu\n",
                           (unsigned long long)win.L, (unsigned long long)win.nwords,
                           (unsigned long long)win.cursor, (unsigned long long)n);
-  const DevPack& hp = DIST == ZF_NORMAL ? t->host.hn : t->host.ex;
-  const uint32_t lmax = (uint32_t)hp.lmax;
+  const DevPack* dP = primary_pack<DIST>(t->dev);  // device address
   const uint64_t L = win.L;
   const uint32_t nb = (uint32_t)((L + kRB - 1) / kRB);
   Workspace ws(s);
@@ -462,7 +460,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   if (debug_on()) fprintf(stderr, "[zf] workspace allocated\n");
   ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
   ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
-  rp_count_exc<<<nb, kRT, 0, s>>>(win, lmax, bcnt);
+  rp_count_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, bcnt);
   dbg("rp_count_exc", s);
   scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt, boff, nb, 0u,
                                                 reinterpret_cast<uint32_t*>(scal));
@@ -483,10 +481,10 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(ws.alloc(&real, m));
   ZF_TRY(ws.alloc(&bmax, nbE));
   ZF_TRY(ws.alloc(&bpre, nbE));
-  rp_compact_exc<<<nb, kRT, 0, s>>>(win, lmax, boff, E);
+  rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E);
   dbg("rp_compact_exc", s);
   if (m) {
-    constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+    constexpr int kPacks = kPacksOf<DIST>;
     const size_t smem = kPacks * sizeof(DevPack);
     ZF_TRY(cudaFuncSetAttribute(rp_draw_exc<DIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
@@ -557,6 +555,7 @@ int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, u
   if (n == 0) return ZF_OK;
   if (!words || nwords == 0 || !out) return ZF_EINVAL;
   if (n >= (1ull << 31)) return ZF_ERANGE;
+  ZF_TRY_STATUS(check_kind(t, dist));
   if (dist == ZF_EXP && dtype == ZF_F64)
     return replay_typed<ZF_EXP, double>(t, words, nwords, cursor, wrap, out, n, recs, counters,
                                         consumed, s);
@@ -569,6 +568,18 @@ int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, u
   if (dist == ZF_NORMAL && dtype == ZF_F32)
     return replay_typed<ZF_NORMAL, float>(t, words, nwords, cursor, wrap, out, n, recs, counters,
                                           consumed, s);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F64)
+    return replay_typed<ZF_TRAD_EXP, double>(t, words, nwords, cursor, wrap, out, n, recs,
+                                             counters, consumed, s);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F32)
+    return replay_typed<ZF_TRAD_EXP, float>(t, words, nwords, cursor, wrap, out, n, recs,
+                                            counters, consumed, s);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F64)
+    return replay_typed<ZF_TRAD_NORMAL, double>(t, words, nwords, cursor, wrap, out, n, recs,
+                                                counters, consumed, s);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F32)
+    return replay_typed<ZF_TRAD_NORMAL, float>(t, words, nwords, cursor, wrap, out, n, recs,
+                                               counters, consumed, s);
   return ZF_EDIST;
 }
 

@@ -101,14 +101,13 @@ __global__ void __launch_bounds__(kThreads)
                       uint64_t n, zf_stats_cfg cfg, double* __restrict__ partials,
                       unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  constexpr int kPacks = kPacksOf<DIST>;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
   StatsShared* sh = reinterpret_cast<StatsShared*>(smem_raw + kPacks * sizeof(DevPack));
   uint32_t* queues = reinterpret_cast<uint32_t*>(sh + 1);
   uint32_t* queue = queues + (threadIdx.x >> 5) * kQueueCap;
   unsigned int* hist = queues + kWarps * kQueueCap;
-  stage_block(sp, DIST == ZF_NORMAL ? (const void*)&gt->hn : (const void*)&gt->ex,
-              kPacks * (int)sizeof(DevPack));
+  stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const int lane = threadIdx.x & 31;
@@ -183,7 +182,7 @@ template <int DIST>
 int launch_fill_stats_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base, uint64_t n,
                            const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,
                            cudaStream_t s) {
-  constexpr int kPacks = DIST == ZF_NORMAL ? 2 : 1;
+  constexpr int kPacks = kPacksOf<DIST>;
   const uint32_t grid = stats_blocks(n);
   const int mode = sum_only(cfg) ? 0 : extra(cfg) ? 2 : 1;
   const size_t smem = kPacks * sizeof(DevPack) + sizeof(StatsShared) +
@@ -207,10 +206,15 @@ int launch_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_
                       const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,
                       cudaStream_t s) {
   ZF_TRY_STATUS(check_cfg(cfg));
+  ZF_TRY_STATUS(check_kind(t, dist));
   if (dist == ZF_EXP)
     return launch_fill_stats_dist<ZF_EXP>(t, seed, ctr_base, n, cfg, partials, counts, s);
   if (dist == ZF_NORMAL)
     return launch_fill_stats_dist<ZF_NORMAL>(t, seed, ctr_base, n, cfg, partials, counts, s);
+  if (dist == ZF_TRAD_EXP)
+    return launch_fill_stats_dist<ZF_TRAD_EXP>(t, seed, ctr_base, n, cfg, partials, counts, s);
+  if (dist == ZF_TRAD_NORMAL)
+    return launch_fill_stats_dist<ZF_TRAD_NORMAL>(t, seed, ctr_base, n, cfg, partials, counts, s);
   return ZF_EDIST;
 }
 

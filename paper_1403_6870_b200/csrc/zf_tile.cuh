@@ -164,7 +164,6 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
   constexpr int V = Sink::V;
   constexpr int kIters = kPerLane / V;
   constexpr uint64_t kIterStride = (uint64_t)(32 * V) * kGamma;  // mod 2^64
-  const uint32_t lmax = (uint32_t)P.lmax;
   const double* sx = P.sx;
   const uint64_t k_lane = base + (uint64_t)lane * V;
   const uint64_t st0 = seed + (ctr_base + k_lane + 1) * kGamma;
@@ -179,7 +178,10 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
         // sx[i+1] is NaN for every byte i >= L_max (see fill_devpack), so the
         // fast value itself flags an exceptional sample: a DSETP on the fp64
         // pipe instead of integer compare/select work on the busy ALU pipe.
-        const double d = fast_value<DIST>(sx, mix13(st + (uint64_t)e * kGamma));
+        const uint64_t w = mix13(st + (uint64_t)e * kGamma);
+        double d = fast_value<DIST>(sx, w);
+        if constexpr (kTrad<DIST>)  // traditional: integer fast-accept test
+          d = trad_fast<DIST>(P.kk, w) ? d : __longlong_as_double(0x7ff8000000000000ll);
         sink.flag(mask, d, 1u << (it * V + e));
         v[e] = to_out<OutT>(d);
       }
@@ -200,7 +202,7 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
         const uint64_t k = k_lane + (uint64_t)it * 32 * V + e;
         if (k < n) {
           const uint64_t u = mix13(st0 + (uint64_t)it * kIterStride + (uint64_t)e * kGamma);
-          const bool exc = ((uint32_t)u & 0xFFu) >= lmax;
+          const bool exc = exc_word<DIST>(P, u);
           mask |= (uint32_t)exc << (it * V + e);
           sink.put(k, to_out<OutT>(fast_value<DIST>(sx, u)), exc);
           ++valid;

@@ -78,22 +78,21 @@ def _alias_for(tables: ZigguratTables):
     return hit[1]
 
 
-class _Sampler:
-    _dist: int
+class _SamplerBase:
+    """Device, source, counters and the fill/launch plumbing shared by the
+    modified samplers and the traditional baseline (`traditional.py`)."""
 
-    def __init__(self, tables, exp_tables, source, device):
+    _dist: int
+    _dev_tables: "_lib.DeviceTables"
+
+    def _init_device(self, source, device) -> None:
         import torch
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("samplers run on CUDA devices only (no CPU fallback)")
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
-        self.tables = tables
-        self.exp_tables = exp_tables
-        self.alias = _alias_for(tables)
         self.source = source if source is not None else UniformSource()
-        hn = tables if tables.distribution == HALF_NORMAL else default_tables(HALF_NORMAL)
-        self._dev_tables = _lib.device_tables(exp_tables, hn, self.device.index)
         self._counters = torch.zeros(6, dtype=torch.int64, device=self.device)
 
     # -- counters ---------------------------------------------------------------
@@ -235,6 +234,18 @@ class _Sampler:
             total.append(buffer_sums(buf, moments=1)[0][0])
             left -= m
         return math.fsum(total)
+
+
+class _Sampler(_SamplerBase):
+    """Modified-ziggurat sampler state: tables, alias, uploaded packs."""
+
+    def __init__(self, tables, exp_tables, source, device):
+        self._init_device(source, device)
+        self.tables = tables
+        self.exp_tables = exp_tables
+        self.alias = _alias_for(tables)
+        hn = tables if tables.distribution == HALF_NORMAL else default_tables(HALF_NORMAL)
+        self._dev_tables = _lib.device_tables(exp_tables, hn, self.device.index)
 
 
 class ExpSampler(_Sampler):

@@ -1,0 +1,235 @@
+"""Traditional (Marsaglia-Tsang) ziggurat baseline on B200.
+
+Mirrors `zigfast/traditional.py:1-207`: the equal-area layer stack solved by
+bisection on the base abscissa r (`solve_traditional`, :56-96), the integer
+fast-accept thresholds (`_int_thresholds`, :99-110), the flat pack (`_pack`,
+:113-121) and the two samplers with the reference's methods (`sample`,
+`sample_counted`, `fill`, `fill_counted`, `aggregate`, `path_counts`,
+`reset_counters`, `fast_accept_fraction`).  The draw bodies run in the sm_100a
+library (dist codes ZF_TRAD_EXP / ZF_TRAD_NORMAL) on the same sources as the
+modified samplers: production counter streams and the reference's exact
+sequential streams (oracle mode).
+
+Counter slots follow `trad_*_counted` (`_kernels.py:956-979, 1117-1146`):
+0 byte words, 1 fast accepts, 2 wedge (density) tests, 3 tail entries.
+
+The tail values are `r - log(u)` (exp) and `r + (-log(u) / r)` (normal): the
+device evaluates log in double-double and rounds once, i.e. the correctly
+rounded log, which is what glibc returns for all but a vanishing fraction of
+arguments; the tests allow 2 ulp on tail samples (north_star's tolerance) and
+require bit equality everywhere else.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import NonConvergence
+from .samplers import _SamplerBase
+from .tables import EXPONENTIAL, HALF_NORMAL
+from .uniform import UniformSource
+
+TWO_64 = 2.0 ** 64
+TWO_63 = 2.0 ** 63
+_SQRT_HALF_PI = math.sqrt(math.pi / 2.0)
+
+
+# -- the two densities (densities.py:41-67), unnormalised with peak 1 ------------
+
+def _density(kind: str):
+    if kind == EXPONENTIAL:
+        return (lambda x: math.exp(-x), lambda x: math.exp(-x), lambda f: -math.log(f))
+    if kind == HALF_NORMAL:
+        return (lambda x: math.exp(-0.5 * x * x),
+                lambda x: _SQRT_HALF_PI * math.erfc(x / math.sqrt(2.0)),
+                lambda f: math.sqrt(-2.0 * math.log(f)))
+    raise ValueError(f"unknown density kind: {kind!r}")
+
+
+def _kind_of(spec) -> str:
+    kind = spec if isinstance(spec, str) else getattr(spec, "kind", None)
+    if kind not in (EXPONENTIAL, HALF_NORMAL):
+        raise ValueError(f"unknown density kind: {kind!r}")
+    return kind
+
+
+@dataclass(frozen=True)
+class TraditionalTables:
+    """Traditional layer stack plus the per-byte fast-accept ratio table
+    (`traditional.py:33-53`)."""
+
+    distribution: str
+    i_max: int
+    r: float
+    v: float          # area of every strip, tail included in strip 0
+    x: np.ndarray     # x[0] = r, x[i] = inverse(f[i]); decreasing
+    f: np.ndarray     # f[0] = density(r), f[i_max - 1] == 1
+    k: np.ndarray     # fast-accept ratios per byte, in [0, 1]
+
+    @property
+    def edge(self) -> np.ndarray:
+        """Per-byte proposal edge length: virtual base edge, then x[i-1]."""
+        e = np.empty(self.i_max)
+        e[0] = self.v / self.f[0]
+        e[1:] = self.x[:-1]
+        return e
+
+    def fast_accept_probability(self) -> float:
+        return float(self.k.mean())
+
+
+def _bisect_to_ulp(fn, lo: float, hi: float) -> float:
+    """Bisection until the bracket has no representable midpoint
+    (`tables.py:107-127`)."""
+    flo, fhi = fn(lo), fn(hi)
+    if flo == 0.0:
+        return lo
+    if fhi == 0.0:
+        return hi
+    if (flo > 0.0) == (fhi > 0.0):
+        raise NonConvergence(f"no sign change on [{lo!r}, {hi!r}]")
+    while True:
+        mid = 0.5 * (lo + hi)
+        if mid <= lo or mid >= hi:
+            return hi if abs(fhi) < abs(flo) else lo
+        fmid = fn(mid)
+        if fmid == 0.0:
+            return mid
+        if (fmid > 0.0) == (flo > 0.0):
+            lo, flo = mid, fmid
+        else:
+            hi, fhi = mid, fmid
+
+
+_SOLVED: dict = {}
+
+
+def solve_traditional(spec, i_max: int = 256, tol: float = 1e-12) -> TraditionalTables:
+    """Find r by bisection so the equal-area stack closes at the peak
+    (`traditional.py:56-96`).  ``spec`` is a density kind or an object with a
+    ``kind`` attribute (the reference's DensitySpec).  Results are cached."""
+    if i_max < 2 or i_max & (i_max - 1):
+        raise ValueError(f"i_max must be a power of two >= 2, got {i_max}")
+    kind = _kind_of(spec)
+    hit = _SOLVED.get((kind, i_max))
+    if hit is not None:
+        return hit
+    density, ccdf, inverse = _density(kind)
+
+    def stack(r: float):
+        f0 = density(r)
+        v = r * f0 + ccdf(r)
+        fs = np.empty(i_max)
+        xs = np.empty(i_max)
+        fs[0], xs[0] = f0, r
+        for i in range(1, i_max):
+            f = fs[i - 1] + v / xs[i - 1]
+            if f >= 1.0 and i < i_max - 1:
+                return None, None, v  # overshot the peak early: r too small
+            fs[i] = f
+            xs[i] = inverse(f) if f < 1.0 else 0.0
+        return fs, xs, v
+
+    def resid(r: float) -> float:
+        fs, _, _ = stack(r)
+        return 1.0 if fs is None else fs[i_max - 1] - 1.0
+
+    try:
+        r = _bisect_to_ulp(resid, 1e-3, inverse(1e-13))
+    except NonConvergence as exc:
+        raise NonConvergence(f"traditional base abscissa for {kind!r}") from exc
+    fs, xs, v = stack(r)
+    if fs is None:
+        raise NonConvergence("stack inconsistent at the converged base abscissa")
+    fs[i_max - 1] = min(fs[i_max - 1], 1.0)
+    k = np.empty(i_max)
+    k[0] = r * fs[0] / v
+    k[1:] = xs[1:] / xs[:-1]
+    if np.any(k < 0.0) or np.any(k > 1.0):
+        raise NonConvergence("fast-accept ratios out of range")
+    t = TraditionalTables(distribution=kind, i_max=i_max, r=float(r), v=float(v), x=xs, f=fs, k=k)
+    _SOLVED[(kind, i_max)] = t
+    return t
+
+
+def _int_thresholds(tables: TraditionalTables, scale: float) -> np.ndarray:
+    """floor(k * scale), nudged down so a fast accept can never overshoot
+    (`traditional.py:99-110`)."""
+    edge = tables.edge
+    bound = np.empty(tables.i_max)
+    bound[0] = tables.r
+    bound[1:] = tables.x[1:]
+    kk = np.floor(tables.k * scale).astype(np.uint64)
+    inv = 1.0 / scale
+    for i in range(tables.i_max):
+        while kk[i] > 0 and np.float64(kk[i]) * inv * edge[i] > bound[i]:
+            kk[i] -= np.uint64(1)
+    return kk
+
+
+@dataclass(frozen=True)
+class TradPack:
+    se: np.ndarray
+    kk: np.ndarray
+    flo: np.ndarray
+    fh: np.ndarray
+    r: float
+
+
+def trad_pack(tables: TraditionalTables) -> TradPack:
+    """`_pack(tables, signed)` (`traditional.py:113-121`): the flat arrays the
+    draw bodies read (signed = half-normal, words scaled by 2^-63)."""
+    scale = TWO_63 if tables.distribution == HALF_NORMAL else TWO_64
+    se = tables.edge * (1.0 / scale)
+    kk = _int_thresholds(tables, scale)
+    flo = np.zeros(tables.i_max)
+    fh = np.zeros(tables.i_max)
+    flo[1:] = tables.f[:-1]
+    fh[1:] = tables.f[1:] - tables.f[:-1]
+    return TradPack(se=se, kk=kk, flo=flo, fh=fh, r=float(tables.r))
+
+
+class _TraditionalSampler(_SamplerBase):
+    """`_TraditionalSampler` (`traditional.py:124-142`) on the device."""
+
+    def __init__(self, kind: str, i_max: int, source: UniformSource | None,
+                 tables: TraditionalTables | None, device):
+        if tables is None:
+            tables = solve_traditional(kind, i_max)
+        if tables.distribution != kind:
+            raise ValueError(f"tables are for {tables.distribution!r}, need {kind!r}")
+        if tables.i_max != 256:
+            raise ValueError("the device kernels index layers by the word's low byte: i_max = 256")
+        self._init_device(source, device)
+        self.tables = tables
+        other = solve_traditional(HALF_NORMAL if kind == EXPONENTIAL else EXPONENTIAL, 256)
+        exp_t, hn_t = (tables, other) if kind == EXPONENTIAL else (other, tables)
+        self._dev_tables = _lib.device_trad_tables(exp_t, hn_t, self.device.index)
+
+    def fast_accept_fraction(self) -> float:
+        c = self.counters
+        return c[1] / c[0] if c[0] else 0.0
+
+
+class TraditionalExpSampler(_TraditionalSampler):
+    """`TraditionalExpSampler` (`traditional.py:145-176`)."""
+
+    _dist = _lib.TRAD_EXP
+
+    def __init__(self, tables: TraditionalTables | None = None,
+                 source: UniformSource | None = None, i_max: int = 256, device=None):
+        super().__init__(EXPONENTIAL, i_max, source, tables, device)
+
+
+class TraditionalNormalSampler(_TraditionalSampler):
+    """`TraditionalNormalSampler` (`traditional.py:179-207`)."""
+
+    _dist = _lib.TRAD_NORMAL
+
+    def __init__(self, tables: TraditionalTables | None = None,
+                 source: UniformSource | None = None, i_max: int = 256, device=None):
+        super().__init__(HALF_NORMAL, i_max, source, tables, device)

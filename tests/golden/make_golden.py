@@ -20,7 +20,11 @@ bit patterns in hex, so comparisons are bit-exact):
   head/tail samples; the same for the normal sampler on the same stream;
 * production ("ctr") stream samples evaluated BY THE REFERENCE through replay
   of each sample's word sequence [S(K), S(2^63 + K*2^19 + t) ...];
-* derive_seed values and aggregate() sums.
+* derive_seed values and aggregate() sums;
+* the traditional baseline (traditional.py, _kernels.py:933-1277): solved
+  tables and packs, golden draws (tests/test_traditional.py:15-29), fills,
+  counters, replay KATs, a config-1-sized record digest and production-stream
+  samples evaluated through replay.
 """
 import hashlib
 import json
@@ -29,7 +33,10 @@ import sys
 
 import numpy as np
 
-from zigfast import ExpSampler, NormalSampler, UniformSource, derive_seed
+from zigfast import (ExpSampler, NormalSampler, TraditionalExpSampler, TraditionalNormalSampler,
+                     UniformSource, derive_seed, solve_traditional)
+from zigfast.densities import exponential, half_normal
+from zigfast.traditional import _pack as trad_pack
 from zigfast._packs import make_alias
 from zigfast.tables import default_tables
 
@@ -91,6 +98,87 @@ def records(cls, words, n):
         path[k] = bits
         att[k] = d[5]
     return vals, starts, nw, layer, path, att, s.counters.copy(), int(s.source.state[0])
+
+
+def trad_records(cls, words, n):
+    """Per-sample records of the traditional samplers (slots 0 draws, 1 fast,
+    2 wedge tests, 3 tails): exit path = tail / fast / wedge accept."""
+    s = cls(source=UniformSource.replay(words))
+    starts = np.empty(n, np.uint64)
+    nw = np.empty(n, np.uint32)
+    layer = np.empty(n, np.uint8)
+    path = np.empty(n, np.uint8)
+    att = np.empty(n, np.uint16)
+    vals = np.empty(n)
+    for k in range(n):
+        p0 = int(s.source.state[0])
+        c0 = s.counters.copy()
+        vals[k] = s.sample_counted()
+        d = s.counters - c0
+        starts[k] = p0
+        nw[k] = int(s.source.state[0]) - p0
+        layer[k] = int(words[p0 % len(words)]) & 0xFF
+        path[k] = 2 if d[3] else (1 if d[1] else 8)
+        att[k] = d[2]
+    return vals, starts, nw, layer, path, att, s.counters.copy(), int(s.source.state[0])
+
+
+def traditional(g, words):
+    for kind, fn, name, cls in (("exponential", exponential, "trad_exp", TraditionalExpSampler),
+                                ("halfnormal", half_normal, "trad_normal",
+                                 TraditionalNormalSampler)):
+        t = solve_traditional(fn(), 256)
+        se, kk, flo, fh, r = trad_pack(t, signed=(kind == "halfnormal"))
+        g[f"{name}_tables"] = {
+            "r": hexbits([t.r])[0], "v": hexbits([t.v])[0], "x_sha256": sha(t.x),
+            "f_sha256": sha(t.f), "k_sha256": sha(t.k), "se_sha256": sha(se),
+            "kk_sha256": sha(kk.astype(np.uint64)), "flo_sha256": sha(flo), "fh_sha256": sha(fh),
+            "kk0": int(kk[0]), "fast_accept_probability": t.fast_accept_probability()}
+        s = cls(source=UniformSource(7))
+        g[f"{name}_seed7_first5"] = hexbits([s.sample() for _ in range(5)])
+        g[f"{name}_seed7_fill3000"] = hexbits(cls(source=UniformSource(7)).fill(3000))
+        g[f"{name}_splitmix99_fill2000"] = hexbits(
+            cls(source=UniformSource(99, generator="splitmix64")).fill(2000))
+        c = cls(source=UniformSource(3))
+        c.fill_counted(200_000)
+        g[f"{name}_seed3_counts200k"] = [int(x) for x in c.counters]
+        g[f"{name}_seed11_aggregate20000"] = hexbits(
+            [cls(source=UniformSource(11)).aggregate(20000)])[0]
+        # replay KATs: fast accept, tail, wedge reject + restart
+        kat = {}
+        for label, w in (("fast", [123456789 << 8]),
+                         ("tail", [0xFFFFFFFFFFFFFF00, 0x0123456789ABCDEF]),
+                         ("tail_neg", [0x8000000000000100 - 0x100, 0x0123456789ABCDEF,
+                                       0xFEDCBA9876543210] * 4),
+                         ("wedge", [0xFFFFFFFFFFFFFF05, 0xFFFFFFFFFFFFFFFF, 42 << 8])):
+            rs = cls(source=UniformSource.replay(w))
+            kat[label] = {"words": [format(x, "016x") for x in w],
+                          "value": hexbits([rs.sample()])[0], "cursor": int(rs.source.state[0])}
+        g[f"{name}_kat"] = kat
+        n1 = 1_000_000
+        vals, starts, nw, layer, path, att, cnt, used = trad_records(cls, words, n1)
+        ref = cls(source=UniformSource(42)).fill(n1)
+        assert np.array_equal(ref.view(np.uint64), vals.view(np.uint64))
+        g[f"c1_{name}"] = {
+            "n": n1, "values_sha256": sha(vals), "starts_sha256": sha(starts),
+            "nwords_sha256": sha(nw), "layer_sha256": sha(layer), "path_sha256": sha(path),
+            "attempts_sha256": sha(att) if name == "trad_exp" else None,
+            "counters": [int(x) for x in cnt], "words_consumed": used,
+            "head": hexbits(vals[:64]), "tail": hexbits(vals[-64:]),
+            "tail_positions": [int(i) for i in np.nonzero(path == 2)[0][:2000]],
+            "n_exceptional": int((nw > 1).sum()),
+        }
+        print(name, "config-1 digests done", cnt, used, file=sys.stderr)
+        out = {}
+        for seed, base, count in ((1234, 0, 4096), (7, 1 << 40, 2048)):
+            vv = []
+            for k in range(count):
+                w = ctr_words(seed, base + k, 64)
+                rs = cls(source=UniformSource.replay(w))
+                vv.append(rs.sample())
+                assert int(rs.source.state[0]) <= len(w)
+            out[f"{seed}:{base}"] = hexbits(vv)
+        g[f"ctr_{name}"] = out
 
 
 def main():
@@ -169,6 +257,7 @@ def main():
             out[f"{seed}:{base}"] = hexbits(vals)
         g[f"ctr_{name}"] = out
 
+    traditional(g, words)
     g["derive_seed"] = {f"{b}:{s}": derive_seed(b, s) for b in (0, 123, 1234, M64) for s in (0, 1, 7)}
     OUT.write_text(json.dumps(g, indent=0))
     print("wrote", OUT, OUT.stat().st_size, "bytes", file=sys.stderr)

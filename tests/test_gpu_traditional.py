@@ -1,0 +1,191 @@
+"""Traditional ziggurat baseline on the GPU (dist codes ZF_TRAD_*): production
+counter stream and oracle mode against the CPU oracle and the reference's own
+fixtures.  Values are bit-exact except tail samples (r - log u), which the
+tests allow to differ by <= 2 ulp (north_star's tolerance; the device log is
+correctly rounded, glibc's nearly always is)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import assert_bits_equal, assert_trad_close, bits, hex_to_bits
+
+pytestmark = pytest.mark.gpu
+
+TRAD = ["trad_exp", "trad_normal"]
+P_TAIL = 2
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def zf(cuda):
+    import paper_1403_6870_b200 as zf
+    return zf
+
+
+def cls_of(zf, dist):
+    return zf.TraditionalExpSampler if dist == "trad_exp" else zf.TraditionalNormalSampler
+
+
+def ctr_sampler(zf, dist, seed, counter=0, device=None):
+    return cls_of(zf, dist)(source=zf.UniformSource.counter(seed, counter), device=device)
+
+
+@pytest.mark.parametrize("dist", TRAD)
+@pytest.mark.parametrize("n", [1, 7, 511, 513, 4096, 100_003])
+def test_production_fill_matches_oracle(zf, orc, cuda, dist, n):
+    got = ctr_sampler(zf, dist, 1234, device=cuda).fill(n).cpu().numpy()
+    want, _, recs = orc.fill_ctr(dist, n, seed=1234, records=True)
+    assert_trad_close(got, bits(want), recs["path"] == P_TAIL, f"{dist} n={n}")
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_production_matches_reference_replay(zf, orc, golden, cuda, dist):
+    for key, want in golden[f"ctr_{dist}"].items():
+        seed, base = (int(x) for x in key.split(":"))
+        got = ctr_sampler(zf, dist, seed, base, device=cuda).fill(len(want)).cpu().numpy()
+        _, _, recs = orc.fill_ctr(dist, len(want), seed=seed, ctr_base=base, records=True)
+        assert_trad_close(got, hex_to_bits(want), recs["path"] == P_TAIL, key)
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_production_counters_and_f32(zf, orc, cuda, dist):
+    import torch
+    s = ctr_sampler(zf, dist, 21, device=cuda)
+    f64 = s.fill_counted(300_000)
+    _, cnt, _ = orc.fill_ctr(dist, 300_000, seed=21)
+    assert s.counters.tolist() == cnt.tolist()
+    out = torch.empty(300_000, dtype=torch.float32, device=cuda)
+    ctr_sampler(zf, dist, 21, device=cuda).fill(out)
+    assert torch.equal(out, f64.to(torch.float32))
+
+
+def test_oracle_mode_golden_first_draws(zf, cuda):
+    """reference tests/test_traditional.py:15-29, 60-62"""
+    from test_traditional_host import GOLDEN_EXP_SEED7, GOLDEN_NORMAL_SEED7
+    e = zf.TraditionalExpSampler(source=zf.UniformSource(7), device=cuda)
+    nrm = zf.TraditionalNormalSampler(source=zf.UniformSource(7), device=cuda)
+    assert [e.sample() for _ in range(5)] == GOLDEN_EXP_SEED7
+    assert [nrm.sample() for _ in range(5)] == GOLDEN_NORMAL_SEED7
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_oracle_mode_fills_and_counts(zf, orc, golden, cuda, dist):
+    cls = cls_of(zf, dist)
+    got = cls(source=zf.UniformSource(7), device=cuda).fill(3000).cpu().numpy()
+    _, _, recs, _ = orc.fill_stream(dist, 3000, seed=7, records=True)
+    assert_trad_close(got, hex_to_bits(golden[f"{dist}_seed7_fill3000"]),
+                      recs["path"] == P_TAIL, "seed 7")
+    got = cls(source=zf.UniformSource(99, generator="splitmix64"), device=cuda).fill(2000)
+    _, _, recs, _ = orc.fill_stream(dist, 2000, generator="splitmix64", seed=99, records=True)
+    assert_trad_close(got.cpu().numpy(), hex_to_bits(golden[f"{dist}_splitmix99_fill2000"]),
+                      recs["path"] == P_TAIL, "splitmix 99")
+    c = cls(source=zf.UniformSource(3), device=cuda)
+    c.fill_counted(200_000)
+    assert c.counters.tolist() == golden[f"{dist}_seed3_counts200k"]
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_fill_equals_scalar_draws(zf, cuda, dist):
+    """reference tests/test_traditional.py:65-76"""
+    cls = cls_of(zf, dist)
+    a, b, c = (cls(source=zf.UniformSource(7), device=cuda) for _ in range(3))
+    block = a.fill(300).cpu().numpy()
+    counted = b.fill_counted(300).cpu().numpy()
+    singles = np.array([c.sample_counted() for _ in range(300)])
+    assert np.array_equal(bits(block), bits(singles))
+    assert np.array_equal(bits(block), bits(counted))
+    assert b.counters.tolist() == c.counters.tolist()
+    assert np.array_equal(a.source.state, c.source.state)
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_oracle_mode_kats(zf, golden, cuda, dist):
+    for label, kat in golden[f"{dist}_kat"].items():
+        w = np.array([int(h, 16) for h in kat["words"]], dtype=np.uint64)
+        s = cls_of(zf, dist)(source=zf.UniformSource.replay(w), device=cuda)
+        v = s.sample()
+        want = np.array([int(kat["value"], 16)], dtype=np.uint64).view(np.float64)
+        tail = label.startswith("tail")
+        assert_trad_close([v], bits(want), [tail], label)
+        assert int(s.source.state[0]) == kat["cursor"], label
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_config1_records(zf, orc, golden, cuda, dist):
+    """n = 1e6 from UniformSource(42): path records bit-exact (SHA-256 of the
+    reference's), values exact except tails, counters and words consumed."""
+    g = golden[f"c1_{dist}"]
+    s = cls_of(zf, dist)(source=zf.UniformSource(42), device=cuda)
+    vals, recs = s.fill_records(g["n"])
+    for f in ("start", "nwords", "layer", "path"):
+        assert sha(recs[f]) == g[f"{'starts' if f == 'start' else f}_sha256"], f
+    if g["attempts_sha256"]:
+        assert sha(recs["attempts"]) == g["attempts_sha256"]
+    want, _, _, _ = orc.fill_stream(dist, g["n"], seed=42)
+    assert_trad_close(vals.cpu().numpy(), bits(want), recs["path"] == P_TAIL, "c1")
+    c = cls_of(zf, dist)(source=zf.UniformSource(42), device=cuda)
+    c.fill_counted(g["n"])
+    assert c.counters.tolist() == g["counters"]
+    ref_state = zf.UniformSource(42)
+    ref_state.jump(g["words_consumed"])
+    assert np.array_equal(c.source.state, ref_state.state)
+
+
+def test_fast_accept_fraction_matches_tables(zf, cuda):
+    """reference tests/test_traditional.py:91-97"""
+    s = zf.TraditionalExpSampler(source=zf.UniformSource.counter(9), device=cuda)
+    s.fill_counted(10_000_000)
+    want = s.tables.fast_accept_probability()
+    got = s.fast_accept_fraction()
+    se = (want * (1.0 - want) / s.counters[0]) ** 0.5
+    assert abs(got - want) < 4.0 * se
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_moments_and_sign(zf, cuda, dist):
+    """Raw moments of 2^26 production draws within 6 sigma (quality.py:31-42),
+    and the normal sign balance (reference tests/test_traditional.py:106-108)."""
+    from paper_1403_6870_b200 import quality
+    n = 1 << 26
+    s = ctr_sampler(zf, dist, 2024, device=cuda)
+    sums, res = quality.device_sums(s, n, thresholds=(0.0,))
+    key = "exp" if dist == "trad_exp" else "normal"
+    for k in range(5):
+        m = sums[k] / n
+        se = quality._MOMENT_SD[key][k] / n ** 0.5
+        assert abs(m - quality.EXPECTED_MOMENTS[key][k]) < 6 * se, k
+    if dist == "trad_normal":
+        assert abs(res.thresh_counts[0] / n - 0.5) < 6 * (0.25 / n) ** 0.5
+
+
+@pytest.mark.parametrize("dist", TRAD)
+def test_aggregate(zf, orc, golden, cuda, dist):
+    import math
+    got = cls_of(zf, dist)(source=zf.UniformSource(11), device=cuda).aggregate(20000)
+    want = np.array([int(golden[f"{dist}_seed11_aggregate20000"], 16)],
+                    dtype=np.uint64).view(np.float64)[0]
+    assert got == pytest.approx(want, rel=1e-12, abs=1e-9)
+    vals, _, _ = orc.fill_ctr(dist, 1_000_000, seed=3)
+    p = ctr_sampler(zf, dist, 3, device=cuda)
+    assert p.aggregate(1_000_000) == pytest.approx(math.fsum(vals.tolist()), rel=1e-12)
+
+
+def test_tables_and_dists_must_match(zf, cuda):
+    import torch
+    from paper_1403_6870_b200 import _lib
+    from paper_1403_6870_b200.errors import DeviceError
+    t = zf.solve_traditional("halfnormal", 256)
+    with pytest.raises(ValueError):
+        zf.TraditionalExpSampler(tables=t, device=cuda)
+    s = ctr_sampler(zf, "trad_exp", 1, device=cuda)
+    out = torch.empty(16, dtype=torch.float64, device=cuda)
+    # a modified-ziggurat dist code on a traditional handle is refused
+    rc = _lib.lib().zf_fill(s._dev_tables.handle, _lib.EXP, _lib.F64, 1, 0, out.data_ptr(), 16,
+                            None, _lib.stream_handle(cuda))
+    assert rc == -6
+    with pytest.raises(DeviceError):
+        _lib.check(rc)

@@ -12,6 +12,10 @@ c5   tail stress, one GPU's share of config 5: N(0,1) n = 2^33, seed 99, counts 
      |x| > 5, 6, 7 and Exp(1) n = 2^33 counts of x > X[1], vs analytic tail mass
      (5-sigma binomial); generate-and-count, nothing materialised
 f32  fp32 production fills (n = 2^28) for both distributions
+trad modified vs traditional ziggurat on the GPU (the paper's Table 1 comparison,
+     reference tests/test_acceptance.py criterion 6): fp64 fills n = 2^28 and
+     generate-and-sum n = 2^32, production counter streams; plus tail-sample
+     agreement of the device log with glibc's over 2^24 draws
 agg  generate-and-aggregate (the reference's bench loop):
      sum of n = 2^32 draws with nothing written to HBM (sum-only kernel), and
      the 5-moment validation kernel; kernel time by CUDA events
@@ -161,6 +165,43 @@ def agg(n=1 << 32):
         sec = ev_time(run)
         row[f"{name}_gbs"] = 8 * m / sec / 1e9
     emit(row)
+
+
+def trad(n=1 << 28, m=1 << 32):
+    import ctypes as C
+    from paper_1403_6870_b200 import _lib
+    sys.path.insert(0, ".")
+    from oracle import oracle as orc
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    for dist, mod_cls, trad_cls, code in (("exp", zf.ExpSampler, zf.TraditionalExpSampler,
+                                           "trad_exp"),
+                                          ("normal", zf.NormalSampler,
+                                           zf.TraditionalNormalSampler, "trad_normal")):
+        row = {"config": "trad", "dist": dist, "n_fill": n, "n_sum": m}
+        for algo, cls in (("modified", mod_cls), ("traditional", trad_cls)):
+            s = cls(source=zf.UniformSource.counter(1234), device=dev)
+            sec = ev_time(lambda: s.fill(out))
+            row[f"{algo}_fill_samples_per_s"] = n / sec
+            cfg = quality._cfg(moments=1)
+            partials, counts = quality._buffers(dev, m, cfg)
+            lib = _lib.lib()
+
+            def run():
+                _lib.check(lib.zf_fill_stats(s._dev_tables.handle, s._dist, 1234, 0, m,
+                                             C.byref(cfg), partials.data_ptr(),
+                                             counts.data_ptr(), _lib.stream_handle(dev)))
+            row[f"{algo}_sum_samples_per_s"] = m / ev_time(run)
+        row["speedup_fill"] = row["modified_fill_samples_per_s"] / row["traditional_fill_samples_per_s"]
+        row["speedup_sum"] = row["modified_sum_samples_per_s"] / row["traditional_sum_samples_per_s"]
+        k = 1 << 24
+        got = trad_cls(source=zf.UniformSource.counter(77), device=dev).fill(k).cpu().numpy()
+        want, _, recs = orc.fill_ctr(code, k, seed=77, records=True)
+        tail = recs["path"] == 2
+        diff = got.view("u8") != want.view("u8")
+        row["tail_check"] = {"draws": k, "tail_samples": int(tail.sum()),
+                             "mismatches": int(diff.sum()),
+                             "non_tail_mismatches": int((diff & ~tail).sum())}
+        emit(row)
 
 
 if __name__ == "__main__":
