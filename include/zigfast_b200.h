@@ -23,6 +23,7 @@
  *   zf_fill_stats      bench_exp / bench_normal + quality sums          _kernels.py:306-393, quality.py:92-106
  *   zf_stats           quality._moment_sums on a device buffer         quality.py:92-106
  *   zf_fill_batch      many (sampler, fill(8192)) requests, one launch  exponential.py:45-50
+ *   zf_format_g17      gen --format text: f"{v:.17g}\n" per value       cli.py:100-120
  */
 #ifndef ZIGFAST_B200_H
 #define ZIGFAST_B200_H
@@ -203,6 +204,18 @@ int zf_xoshiro_pow2_poly(int e, uint64_t* out4);
 
 /* Batched production fill: one launch for all requests (requests in host
  * memory, copied by the call).  dtype applies to all requests. */
+/* Text output of the reference's `gen --format text` (cli.py:100-120):
+ * writes "".join(f"{v:.17g}\n" for v in x) -- byte-identical to CPython's
+ * '%.17g' -- for n doubles at x_dev into out_dev (capacity `cap` bytes;
+ * 24 * n always suffices).  scratch_dev holds zf_format_scratch_words(n)
+ * uint64 words; on completion scratch_dev[0] = total bytes and
+ * scratch_dev[1] = values outside the supported domain (0 and
+ * 1e-22 <= |v| < 1e17, which contains every sampler output; such values are
+ * skipped).  If the total exceeds cap nothing is written.  Asynchronous. */
+int zf_format_g17(const double* x_dev, uint64_t n, char* out_dev, uint64_t cap,
+                  uint64_t* scratch_dev, void* stream);
+uint64_t zf_format_scratch_words(uint64_t n);
+
 int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                   void* out_dev, void* stream);
 

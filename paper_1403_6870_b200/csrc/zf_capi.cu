@@ -282,6 +282,17 @@ int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* stat
   return ZF_ERANGE;
 }
 
+uint64_t zf_format_scratch_words(uint64_t n) {
+  const uint64_t nb = format_blocks(n);
+  return 2 + (nb + 1) + (nb + 1) / 2;
+}
+
+int zf_format_g17(const double* x_dev, uint64_t n, char* out_dev, uint64_t cap,
+                  uint64_t* scratch_dev, void* stream) {
+  if (!scratch_dev || (n && (!x_dev || !out_dev))) return ZF_EINVAL;
+  return launch_format_g17(x_dev, n, out_dev, cap, scratch_dev, as_stream(stream));
+}
+
 int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                   void* out_dev, void* stream) {
   if (!t || (nreq > 0 && (!reqs || !out_dev))) return ZF_EINVAL;

@@ -58,6 +58,10 @@ int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, u
                uint64_t cursor, int wrap, void* out, uint64_t n, zf_path_rec* recs,
                int64_t* counters, uint64_t* consumed, cudaStream_t s);
 int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cudaStream_t s);
+// launchers (zf_format.cu)
+uint64_t format_blocks(uint64_t n);
+int launch_format_g17(const double* x, uint64_t n, char* out, uint64_t cap, uint64_t* scratch,
+                      cudaStream_t s);
 // xoshiro jump-ahead (zf_jump.cpp)
 void xoshiro_jump_host(uint64_t st[4], uint64_t k);
 // polynomials x^(B * 2^i) mod P for i in [0, levels): levels x 4 words

@@ -16,6 +16,9 @@ trad modified vs traditional ziggurat on the GPU (the paper's Table 1 comparison
      reference tests/test_acceptance.py criterion 6): fp64 fills n = 2^28 and
      generate-and-sum n = 2^32, production counter streams; plus tail-sample
      agreement of the device log with glibc's over 2^24 draws
+fmt  output formats: device '%.17g' text of 2^26 normal draws
+     (kernel time, bytes/s of text) vs CPython's f-string join on a 2^20 sample,
+     and gen-style end to end (fill + format + D2H) into host memory
 agg  generate-and-aggregate (the reference's bench loop):
      sum of n = 2^32 draws with nothing written to HBM (sum-only kernel), and
      the 5-moment validation kernel; kernel time by CUDA events
@@ -202,6 +205,40 @@ def trad(n=1 << 28, m=1 << 32):
                              "mismatches": int(diff.sum()),
                              "non_tail_mismatches": int((diff & ~tail).sum())}
         emit(row)
+
+
+def fmt(n=1 << 26):
+    import ctypes as C
+    from paper_1403_6870_b200 import _lib
+    from paper_1403_6870_b200.output import format_g17
+    s = zf.NormalSampler(source=zf.UniformSource.counter(1), device=dev)
+    x = s.fill(n)
+    out = torch.empty(24 * n, dtype=torch.uint8, device=dev)
+    scratch = torch.zeros(int(_lib.lib().zf_format_scratch_words(n)), dtype=torch.int64,
+                          device=dev)
+    lib = _lib.lib()
+
+    def run():
+        _lib.check(lib.zf_format_g17(x.data_ptr(), n, out.data_ptr(), out.numel(),
+                                     scratch.data_ptr(), _lib.stream_handle(dev)))
+    sec = ev_time(run)
+    nbytes = int(scratch[0].item())
+    sample = x[: 1 << 20].cpu().numpy()
+    t = time.perf_counter()
+    txt = "".join(f"{v:.17g}\n" for v in sample.tolist()).encode()
+    cpu = (1 << 20) / (time.perf_counter() - t)
+    assert format_g17(x[: 1 << 20]).cpu().numpy().tobytes() == txt
+    host = torch.empty(24 * (1 << 24), dtype=torch.uint8).pin_memory()
+
+    def e2e():
+        vals = s.fill(1 << 24)
+        b = format_g17(vals)
+        host[: b.numel()].copy_(b)
+    e2e_sec = wall(e2e)
+    emit({"config": "fmt", "n": n, "text_bytes": nbytes, "bytes_per_value": nbytes / n,
+          "device_values_per_s": n / sec, "device_text_gbs": nbytes / sec / 1e9,
+          "cpython_fstring_values_per_s": cpu,
+          "gen_e2e_values_per_s": (1 << 24) / e2e_sec})
 
 
 if __name__ == "__main__":
