@@ -264,8 +264,7 @@ __device__ __forceinline__ int alias_pick(const DevPack& p, S& s) {
 // Exponential draw whose first byte word `u` has already been taken from the
 // stream (exp_one_counted, _kernels.py:184-223).
 template <class S, class C>
-__device__ double exp_draw(const DevPack& p, uint64_t u, S& s, C& c) {
-  double shift = 0.0;
+__device__ double exp_draw(const DevPack& p, uint64_t u, S& s, C& c, double shift = 0.0) {
   for (;;) {
     c.add(0);
     const int i = (int)(u & 0xFF);

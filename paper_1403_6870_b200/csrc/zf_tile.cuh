@@ -230,7 +230,10 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
   return;
 #endif
   const uint64_t K = ctr_base + k;
-  const uint64_t u = mix13(seed + (K + 1) * kGamma);
+  // k is exceptional: the modified exponential draw only needs to know that
+  // (its first word's bits are never read again), the normal one needs the
+  // sign bit, the traditional ones the whole word
+  const uint64_t u = DIST == ZF_EXP ? 0xFFull : mix13(seed + (K + 1) * kGamma);
   CtrStream s{seed + (kExcBase + (K << kExcShift)) * kGamma};
   double v;
   if (COUNTED) {
@@ -259,6 +262,20 @@ __device__ __forceinline__ int warp_excl_scan(int mine, int lane, int* total) {
   }
   *total = __shfl_sync(0xffffffffu, incl, 31);
   return incl - mine;
+}
+
+// The same prefix from bit-plane ballots: counts are tiny (a lane holds ~0.19
+// exceptional samples per tile), so planes 0 and 1 decide it unless some lane
+// has 4 or more, which falls back to the shuffle scan.  No dependent shuffle
+// chain after pass 1: three independent ballots and a few popcounts.
+__device__ __forceinline__ int warp_excl_count(int mine, int lane, int* total) {
+  const uint32_t b0 = __ballot_sync(0xffffffffu, mine & 1);
+  const uint32_t b1 = __ballot_sync(0xffffffffu, mine & 2);
+  const uint32_t big = __ballot_sync(0xffffffffu, mine >= 4);
+  if (big) return warp_excl_scan(mine, lane, total);
+  const uint32_t lt = (1u << lane) - 1u;
+  *total = __popc(b0) + 2 * __popc(b1);
+  return __popc(b0 & lt) + 2 * __popc(b1 & lt);
 }
 
 template <int V>
@@ -330,7 +347,15 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       const uint32_t mask =
           fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
       int total;
+#ifdef ZF_SHFL_SCAN
       int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
+#else
+      int slot = qn + warp_excl_count(__popc(mask), lane, &total);
+#endif
+#if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 1  // cost isolation: scan only
+      if (total == 12345) q[lane] = slot;
+      continue;
+#endif
       if (total == 0) continue;
       if (qn + total > kQueueCap) {
         // (practically never: ~100 exceptions in one tile, expected ~15) resolve
@@ -346,6 +371,10 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         q[slot++] = (iter << kTileBits) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
       qn += total;
       __syncwarp();
+#if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 2  // cost isolation: scan + enqueue, no rounds
+      if (qn >= 32) qn = 0;
+      continue;
+#endif
       if (qn < 32) continue;
       int done = 0;
       for (; qn - done >= 32; done += 32)
