@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "zf_internal.h"
@@ -59,20 +60,26 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
 }
 
 // ---------------------------------------------------------------------------
-// batched requests (config 4): one launch, tiles mapped to requests through a
-// prefix table of per-request tile counts; both packs staged.
+// batched requests (config 4): one launch; every request is cut into chunks
+// of kBatchChunk tiles, a warp takes whole chunks (chunk -> request from a
+// host-built map, one load) and runs them like a fill -- the per-warp queue
+// spans the chunk's tiles, so pass-2 rounds are mostly full.  Both packs
+// staged; one resident wave so every warp gets ~equal numbers of chunks.
 // ---------------------------------------------------------------------------
+
+constexpr int kBatchChunk = 4;  // tiles per chunk (2048 samples at kTile 512)
 
 struct DevRequest {
   uint64_t seed, ctr_base, n, out_offset;
-  uint64_t tile_begin;  // prefix of tiles
+  uint64_t chunk_begin;  // prefix of chunks
   int32_t dist, pad;
 };
 
 template <typename OutT, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     fill_batch_kernel(const DevTables* __restrict__ gt, const DevRequest* __restrict__ reqs,
-                      int nreq, uint64_t total_tiles, OutT* __restrict__ out) {
+                      const uint32_t* __restrict__ chunk_req, uint64_t total_chunks,
+                      OutT* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DevTables* st = reinterpret_cast<DevTables*>(smem_raw);
   stage_block(st, gt, (int)sizeof(DevTables));
@@ -82,22 +89,19 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   LaneCounts lc;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); tile < total_tiles;
-       tile += nw) {
-    int lo = 0, hi = nreq - 1;  // last request with tile_begin <= tile
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&reqs[mid].tile_begin) <= tile) lo = mid; else hi = mid - 1;
-    }
-    const DevRequest r = reqs[lo];
-    const uint64_t base = (tile - r.tile_begin) * kTile;
+  for (uint64_t chunk = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); chunk < total_chunks;
+       chunk += nw) {
+    const DevRequest r = reqs[__ldg(chunk_req + chunk)];
+    const uint64_t t0 = (chunk - r.chunk_begin) * kBatchChunk;
+    // tiles [t0, t0 + kBatchChunk) of the request: cap n at the chunk's end
+    const uint64_t n_eff = std::min<uint64_t>(r.n, (t0 + kBatchChunk) * kTile);
     StoreSink<OutT, VEC> sink{out + r.out_offset};
     if (r.dist == ZF_EXP)
-      fill_tile<ZF_EXP, false>(st->ex, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue,
-                               kQueueCap, lane, lc);
+      run_tiles<ZF_EXP, false, 3>(st->ex, st->ex, r.seed, r.ctr_base, sink, n_eff, t0, 1, queue,
+                                  lane, lc);
     else
-      fill_tile<ZF_NORMAL, false>(st->hn, st->ex, r.seed, r.ctr_base, sink, r.n, base, queue,
-                                  kQueueCap, lane, lc);
+      run_tiles<ZF_NORMAL, false, 3>(st->hn, st->ex, r.seed, r.ctr_base, sink, n_eff, t0, 1,
+                                     queue, lane, lc);
   }
 }
 
@@ -106,7 +110,8 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 
 template <typename K>
-static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid) {
+static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid,
+                    int fixed_waves = 0) {
   static_assert(sizeof(K) > 0, "");
   int per_sm = 0;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -122,7 +127,8 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
     const char* e = getenv("ZF_GRID_WAVES");
     return e ? std::max(1, atoi(e)) : 4;
   }();
-  *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count * waves);
+  *grid = (int)std::min<uint64_t>(want,
+                                  (uint64_t)per_sm * sm_count * (fixed_waves ? fixed_waves : waves));
   if (*grid < 1) *grid = 1;
   return ZF_OK;
 }
@@ -190,13 +196,15 @@ int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t
 }
 
 template <typename OutT, bool VEC>
-static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq, int nreq,
-                              uint64_t total_tiles, OutT* out, cudaStream_t s) {
+static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq,
+                              const uint32_t* chunk_req, uint64_t total_chunks, OutT* out,
+                              cudaStream_t s) {
   auto kernel = fill_batch_kernel<OutT, VEC>;
   const size_t smem = sizeof(DevTables) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
   int grid = 0;
-  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_tiles, &grid));
-  kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, nreq, total_tiles, out);
+  // one resident wave: every warp loops over ~equal numbers of whole chunks
+  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_chunks, &grid, 1));
+  kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, chunk_req, total_chunks, out);
   return cuda_status(cudaGetLastError());
 }
 
@@ -209,29 +217,40 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
   // every request must keep 16-byte alignment for the vector path
   bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   std::vector<DevRequest> h((size_t)nreq);
-  uint64_t tiles = 0;
+  uint64_t chunks = 0;
   for (int i = 0; i < nreq; ++i) {
     const zf_request& r = reqs[i];
     if (r.dist != ZF_EXP && r.dist != ZF_NORMAL) return ZF_EDIST;
     if (r.ctr_base > kMaxCtr || r.n > kMaxCtr - r.ctr_base) return ZF_ERANGE;
     if ((r.out_offset * esz) & 15) vec = false;
-    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, tiles, r.dist, 0};
-    tiles += (r.n + kTile - 1) / kTile;
+    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, chunks, r.dist, 0};
+    chunks += ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;  // chunks
   }
-  if (tiles == 0) return ZF_OK;
-  DevRequest* d = nullptr;
-  ZF_TRY(cudaMallocAsync(&d, sizeof(DevRequest) * nreq, s));
-  // pageable source: the runtime stages it before returning, so `h` may die
-  cudaError_t e = cudaMemcpyAsync(d, h.data(), sizeof(DevRequest) * nreq,
-                                  cudaMemcpyHostToDevice, s);
+  if (chunks == 0) return ZF_OK;
+  if (chunks > 0xFFFFFFFFull) return ZF_ERANGE;
+  // one upload: the request table, then the chunk -> request map
+  const size_t req_bytes = sizeof(DevRequest) * (size_t)nreq;
+  std::vector<unsigned char> blob(req_bytes + sizeof(uint32_t) * chunks);
+  std::memcpy(blob.data(), h.data(), req_bytes);
+  uint32_t* cmap = reinterpret_cast<uint32_t*>(blob.data() + req_bytes);
+  for (int i = 0; i < nreq; ++i) {
+    const uint64_t end = i + 1 < nreq ? h[i + 1].chunk_begin : chunks;
+    for (uint64_t c = h[i].chunk_begin; c < end; ++c) cmap[c] = (uint32_t)i;
+  }
+  unsigned char* d = nullptr;
+  ZF_TRY(cudaMallocAsync(&d, blob.size(), s));
+  // pageable source: the runtime stages it before returning, so `blob` may die
+  cudaError_t e = cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, s);
   int status = (int)e;
   if (e == cudaSuccess) {
+    const DevRequest* dr = reinterpret_cast<const DevRequest*>(d);
+    const uint32_t* dm = reinterpret_cast<const uint32_t*>(d + req_bytes);
     if (dtype == ZF_F64)
-      status = vec ? launch_batch_typed<double, true>(t, d, nreq, tiles, (double*)out, s)
-                   : launch_batch_typed<double, false>(t, d, nreq, tiles, (double*)out, s);
+      status = vec ? launch_batch_typed<double, true>(t, dr, dm, chunks, (double*)out, s)
+                   : launch_batch_typed<double, false>(t, dr, dm, chunks, (double*)out, s);
     else
-      status = vec ? launch_batch_typed<float, true>(t, d, nreq, tiles, (float*)out, s)
-                   : launch_batch_typed<float, false>(t, d, nreq, tiles, (float*)out, s);
+      status = vec ? launch_batch_typed<float, true>(t, dr, dm, chunks, (float*)out, s)
+                   : launch_batch_typed<float, false>(t, dr, dm, chunks, (float*)out, s);
   }
   cudaFreeAsync(d, s);
   return status;

@@ -283,32 +283,6 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
   return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
 }
 
-// One warp tile with its exceptions resolved immediately (the batch kernel,
-// whose consecutive tiles belong to different requests).  queue: cap u32.
-template <int DIST, bool COUNTED, class Sink>
-__device__ __forceinline__ void fill_tile(const DevPack& P, const DevPack& E, uint64_t seed,
-                                          uint64_t ctr_base, Sink& sink, uint64_t n,
-                                          uint64_t base, uint32_t* queue, int cap, int lane,
-                                          LaneCounts& lc) {
-  const uint32_t mask = fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, base, lane, lc);
-  int total;
-  int slot = warp_excl_scan(__popc(mask), lane, &total);
-  if (total == 0) return;  // warp-uniform
-  if (total > cap) {  // (practically never) resolve in place from the lane masks
-    for (uint32_t m = mask; m; m &= m - 1)
-      resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink,
-                                 base + mask_bit_offset<Sink::V>(__ffs(m) - 1, lane), lc);
-    __syncwarp();
-    return;
-  }
-  for (uint32_t m = mask; m; m &= m - 1)
-    queue[slot++] = mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
-  __syncwarp();
-  for (int j = lane; j < total; j += 32)
-    resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, base + queue[j], lc);
-  __syncwarp();
-}
-
 // Per-warp queue words: < 32 leftovers + the exceptions of one tile (~15 on
 // average for 1024 samples); a tile that would overflow is resolved in place.
 // Small on purpose: shared memory, not registers, limits CTAs per SM.
