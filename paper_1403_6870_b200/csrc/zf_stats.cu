@@ -17,7 +17,10 @@
 namespace zf {
 namespace {
 
-constexpr uint32_t kMaxStatBlocks = 148 * 8;
+#ifndef ZF_STAT_BLOCKS
+#define ZF_STAT_BLOCKS (148 * 8)
+#endif
+constexpr uint32_t kMaxStatBlocks = ZF_STAT_BLOCKS;
 constexpr int kMaxBins = 4096;
 
 // Block scratch; the histogram (nbins + 2 u32) follows it in dynamic shared
