@@ -176,27 +176,31 @@ class DeviceTradTables(DeviceTables):
 
 
 _tables_cache: dict = {}
+_tables_lock = threading.Lock()
+
+
+def _cached_upload(key, exp_tables, hn_tables, make):
+    """One upload per (tables pair, device), shared by every sampler and host
+    thread (the handle is immutable and thread-safe)."""
+    with _tables_lock:
+        hit = _tables_cache.get(key)
+        if hit is None or hit[0] is not exp_tables or hit[1] is not hn_tables:
+            hit = (exp_tables, hn_tables, make())
+            _tables_cache[key] = hit
+        return hit[2]
 
 
 def device_tables(exp_tables, hn_tables, device_index: int) -> DeviceTables:
     """Cached upload of a (exp, half-normal) table pair to a device."""
     from .tables import make_pack
-    key = (id(exp_tables), id(hn_tables), device_index)
-    hit = _tables_cache.get(key)
-    if hit is None or hit[0] is not exp_tables or hit[1] is not hn_tables:
-        dt = DeviceTables(make_pack(exp_tables), make_pack(hn_tables), device_index)
-        hit = (exp_tables, hn_tables, dt)
-        _tables_cache[key] = hit
-    return hit[2]
+    return _cached_upload((id(exp_tables), id(hn_tables), device_index), exp_tables, hn_tables,
+                          lambda: DeviceTables(make_pack(exp_tables), make_pack(hn_tables),
+                                               device_index))
 
 
 def device_trad_tables(exp_tables, hn_tables, device_index: int) -> DeviceTradTables:
     """Cached upload of a traditional (exp, half-normal) table pair."""
     from .traditional import trad_pack
-    key = ("trad", id(exp_tables), id(hn_tables), device_index)
-    hit = _tables_cache.get(key)
-    if hit is None or hit[0] is not exp_tables or hit[1] is not hn_tables:
-        dt = DeviceTradTables(trad_pack(exp_tables), trad_pack(hn_tables), device_index)
-        hit = (exp_tables, hn_tables, dt)
-        _tables_cache[key] = hit
-    return hit[2]
+    return _cached_upload(("trad", id(exp_tables), id(hn_tables), device_index), exp_tables,
+                          hn_tables, lambda: DeviceTradTables(trad_pack(exp_tables),
+                                                              trad_pack(hn_tables), device_index))
