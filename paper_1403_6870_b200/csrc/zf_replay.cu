@@ -87,6 +87,74 @@ struct Max {
   __device__ T operator()(T a, T b) const { return a > b ? a : b; }
 };
 
+// ---- warp-striped position layout --------------------------------------------
+// Block b covers positions [b*kRB, (b+1)*kRB); warp w the span of 32*kRI
+// positions starting at b*kRB + w*32*kRI, item j of lane l being position
+// span + 32*j + l: every load is a coalesced row, order is position order, and
+// prefix counts come from ballots.
+constexpr int kWarpSpan = 32 * kRI;
+
+__device__ __forceinline__ uint64_t striped_pos(int j) {
+  return (uint64_t)blockIdx.x * kRB + (uint64_t)(threadIdx.x >> 5) * kWarpSpan + 32 * j +
+         (threadIdx.x & 31);
+}
+
+// This thread's kRI striped words (0 past the window).  Windows that do not
+// wrap (every sequential-generator fill) take a branch-free path so all kRI
+// loads are in flight together; wrapping replay lists use the modulo.
+__device__ __forceinline__ void load_striped(const Window& win, uint64_t w[kRI]) {
+  const unsigned long long* base = reinterpret_cast<const unsigned long long*>(win.w);
+  if (win.cursor + win.L <= win.nwords) {
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) {
+      const uint64_t p = striped_pos(j);
+      w[j] = p < win.L ? __ldg(base + win.cursor + p) : 0;
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < kRI; ++j) {
+      const uint64_t p = striped_pos(j);
+      w[j] = p < win.L ? win.word(p) : 0;
+    }
+  }
+}
+
+// the same for two counts at once (one pair of barriers)
+__device__ __forceinline__ void warp_base2(uint32_t ta, uint32_t tb, uint2* smem, uint32_t* ba,
+                                           uint32_t* bb) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) smem[wid] = make_uint2(ta, tb);
+  __syncthreads();
+  uint32_t a = 0, b = 0;
+#pragma unroll
+  for (int w = 0; w < kRT / 32; ++w) {
+    const uint2 t = smem[w];
+    a += w < wid ? t.x : 0;
+    b += w < wid ? t.y : 0;
+  }
+  *ba = a;
+  *bb = b;
+  __syncthreads();
+}
+
+// exclusive prefix of per-warp totals over the block's warps (+ block total)
+__device__ __forceinline__ uint32_t warp_base(uint32_t warp_total, uint32_t* smem,
+                                              uint32_t* block_total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) smem[wid] = warp_total;
+  __syncthreads();
+  uint32_t base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kRT / 32; ++w) {
+    const uint32_t t = smem[w];
+    base += w < wid ? t : 0;
+    tot += t;
+  }
+  if (block_total) *block_total = tot;
+  __syncthreads();
+  return base;
+}
+
 // single-block exclusive scan over `cnt` entries (1024 threads)
 template <typename T, class Op>
 __global__ void scan_single(const T* __restrict__ in, T* __restrict__ out, uint64_t cnt,
@@ -110,38 +178,43 @@ __global__ void scan_single(const T* __restrict__ in, T* __restrict__ out, uint6
 
 // ---- A: classify / compact ---------------------------------------------------
 template <int DIST>
-__global__ void rp_count_exc(Window win, const DevPack* __restrict__ P,
-                             uint32_t* __restrict__ bcnt) {
-  __shared__ uint32_t wb[32];
-  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+__global__ void __launch_bounds__(kRT)
+    rp_count_exc(Window win, const DevPack* __restrict__ P, uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t wb[kRT / 32];
+  // all kRI loads in flight before the first ballot (a ballot per load would
+  // serialise them: ~3 TB/s instead of the HBM rate)
+  uint64_t w[kRI];
+  load_striped(win, w);
   uint32_t c = 0;
 #pragma unroll
-  for (int j = 0; j < kRI; ++j) {
-    const uint64_t p = p0 + j;
-    if (p < win.L) c += exc_word<DIST>(*P, win.word(p));
-  }
+  for (int j = 0; j < kRI; ++j)
+    c += __popc(__ballot_sync(0xffffffffu, striped_pos(j) < win.L && exc_word<DIST>(*P, w[j])));
   uint32_t tot;
-  block_exclusive<uint32_t>(c, 0u, Add(), wb, &tot);
+  warp_base(c, wb, &tot);
   if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
 }
 
 template <int DIST>
-__global__ void rp_compact_exc(Window win, const DevPack* __restrict__ P,
-                               const uint32_t* __restrict__ boff, uint32_t* __restrict__ E) {
-  __shared__ uint32_t wb[32];
-  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
-  uint32_t flags = 0, c = 0;
+__global__ void __launch_bounds__(kRT)
+    rp_compact_exc(Window win, const DevPack* __restrict__ P, const uint32_t* __restrict__ boff,
+                   uint32_t* __restrict__ E) {
+  __shared__ uint32_t wb[kRT / 32];
+  const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
+  uint64_t w[kRI];
+  load_striped(win, w);
+  uint32_t b[kRI];
+  uint32_t c = 0;
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const uint64_t p = p0 + j;
-    const uint32_t f = p < win.L && exc_word<DIST>(*P, win.word(p));
-    flags |= f << j;
-    c += f;
+    b[j] = __ballot_sync(0xffffffffu, striped_pos(j) < win.L && exc_word<DIST>(*P, w[j]));
+    c += __popc(b[j]);
   }
-  uint32_t o = boff[blockIdx.x] + block_exclusive<uint32_t>(c, 0u, Add(), wb, nullptr);
+  uint32_t o = boff[blockIdx.x] + warp_base(c, wb, nullptr);
 #pragma unroll
-  for (int j = 0; j < kRI; ++j)
-    if ((flags >> j) & 1) E[o++] = (uint32_t)(p0 + j);
+  for (int j = 0; j < kRI; ++j) {
+    if ((b[j] >> (threadIdx.x & 31)) & 1) E[o + __popc(b[j] & lt)] = (uint32_t)striped_pos(j);
+    o += __popc(b[j]);
+  }
 }
 
 // ---- B: exceptional draws ------------------------------------------------------
@@ -238,16 +311,20 @@ __global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restri
   for (uint64_t q = p + 1; q < stop; ++q) interior[q] = 1;
 }
 
-__global__ void rp_count_starts(const uint8_t* __restrict__ interior, uint64_t L,
-                                uint32_t* __restrict__ bcnt) {
-  __shared__ uint32_t wb[32];
-  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
+__global__ void __launch_bounds__(kRT)
+    rp_count_starts(const uint8_t* __restrict__ interior, uint64_t L, uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t wb[kRT / 32];
+  uint8_t v[kRI];
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const uint64_t p = striped_pos(j);
+    v[j] = p < L ? interior[p] : 1;
+  }
   uint32_t c = 0;
 #pragma unroll
-  for (int j = 0; j < kRI; ++j)
-    if (p0 + j < L) c += interior[p0 + j] == 0;
+  for (int j = 0; j < kRI; ++j) c += __popc(__ballot_sync(0xffffffffu, v[j] == 0));
   uint32_t tot;
-  block_exclusive<uint32_t>(c, 0u, Add(), wb, &tot);
+  warp_base(c, wb, &tot);
   if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
 }
 
@@ -269,51 +346,58 @@ struct EmitArgs {
 template <int DIST, typename OutT>
 __global__ void __launch_bounds__(kRT)
     rp_emit(const DevTables* __restrict__ gt, Window win, EmitArgs a, OutT* __restrict__ out) {
-  __shared__ uint32_t wb[32];
-  __shared__ double sx[kSlots + 2];
+  __shared__ uint2 wb[kRT / 32];
   const DevPack* P = primary_pack<DIST>(gt);
-  for (int i = threadIdx.x; i < kSlots + 2; i += blockDim.x) sx[i] = P->sx[i];
-  __syncthreads();
-  const uint64_t p0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
-  uint32_t ex_flags = 0, st_flags = 0, ce = 0, cs = 0;
+  const double* sx = P->sx;  // 2 KB, L1-resident: no per-block staging barrier
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
   uint64_t wds[kRI];
+  uint8_t inter[kRI];
+  load_striped(win, wds);
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const uint64_t p = p0 + j;
-    wds[j] = 0;
-    if (p < win.L) {
-      wds[j] = win.word(p);
-      const uint32_t e = exc_word<DIST>(*P, wds[j]);
-      const uint32_t s = a.interior[p] == 0;
-      ex_flags |= e << j;
-      st_flags |= s << j;
-      ce += e;
-      cs += s;
-    }
+    const uint64_t p = striped_pos(j);
+    inter[j] = p < win.L ? a.interior[p] : 1;
   }
-  uint32_t eidx = a.boff_exc[blockIdx.x] + block_exclusive<uint32_t>(ce, 0u, Add(), wb, nullptr);
-  uint32_t rank = a.boff_start[blockIdx.x] + block_exclusive<uint32_t>(cs, 0u, Add(), wb, nullptr);
+  uint32_t be[kRI], bs[kRI];
+  uint32_t ce = 0, cs = 0;
+#pragma unroll
+  for (int j = 0; j < kRI; ++j) {
+    const bool in = striped_pos(j) < win.L;
+    be[j] = __ballot_sync(0xffffffffu, in && exc_word<DIST>(*P, wds[j]));
+    bs[j] = __ballot_sync(0xffffffffu, inter[j] == 0);
+    ce += __popc(be[j]);
+    cs += __popc(bs[j]);
+  }
+  uint32_t eidx, rank;
+  warp_base2(ce, cs, wb, &eidx, &rank);
+  eidx += a.boff_exc[blockIdx.x];
+  rank += a.boff_start[blockIdx.x];
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const bool is_ex = (ex_flags >> j) & 1, is_st = (st_flags >> j) & 1;
-    if (is_st && rank < a.n) {
-      const uint64_t p = p0 + j;
+    const bool is_ex = (be[j] >> lane) & 1, is_st = (bs[j] >> lane) & 1;
+    const uint32_t e_i = eidx + __popc(be[j] & lt), r_i = rank + __popc(bs[j] & lt);
+    if (is_st && r_i < a.n) {
+      const uint64_t p = striped_pos(j);
       double v;
       uint32_t nw = 1, meta;
       if (is_ex) {
-        nw = a.len[eidx];
-        v = a.val[eidx];
-        meta = a.meta[eidx];
-        for (int q = 0; q < 6; ++q) c[q] += a.cnt[(uint64_t)eidx * 6 + q];
+        nw = a.len[e_i];
+        v = a.val[e_i];
+        meta = a.meta[e_i];
+        if (a.counters)
+          for (int q = 0; q < 6; ++q) c[q] += a.cnt[(uint64_t)e_i * 6 + q];
       } else {
-        v = fast_value<DIST>(sx, wds[j]);
+        v = __dmul_rn(kSigned<DIST> ? __ll2double_rn((long long)wds[j])
+                                    : __ull2double_rn(wds[j]),
+                      __ldg(sx + (wds[j] & 0xFF) + 1));
         meta = ((uint32_t)wds[j] & 0xFF) | (ZF_PATH_FAST << 8);
         c[0] += 1;
         c[1] += 1;
       }
       if (nw != kIncomplete) {
-        out[rank] = to_out<OutT>(v);
+        out[r_i] = to_out<OutT>(v);
         if (a.recs) {
           zf_path_rec r;
           r.start = p;
@@ -321,18 +405,20 @@ __global__ void __launch_bounds__(kRT)
           r.layer = (uint8_t)(meta & 0xFF);
           r.path = (uint8_t)((meta >> 8) & 0xFF);
           r.attempts = (uint16_t)(meta >> 16);
-          a.recs[rank] = r;
+          a.recs[r_i] = r;
         }
-        if (rank + 1 == a.n) *a.consumed = p + nw;
+        if (r_i + 1 == a.n) *a.consumed = p + nw;
       }
     }
-    eidx += is_ex;
-    rank += is_st;
+    eidx += __popc(be[j]);
+    rank += __popc(bs[j]);
   }
-  for (int q = 0; q < 6; ++q) {
-    unsigned long long v = c[q];
-    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.counters + q, v);
+  if (a.counters) {  // counted fills only: 6 atomics per warp on 6 addresses
+    for (int q = 0; q < 6; ++q) {
+      unsigned long long v = c[q];
+      for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.counters + q, v);
+    }
   }
 }
 
@@ -359,11 +445,37 @@ __device__ __forceinline__ void xo_step(uint64_t s[4]) {
 }
 
 constexpr int kXoBlock = 1024;  // words per thread
-constexpr int kXoLevels = 40;
+constexpr int kXoLevels = 10;   // radix-16 digits of the thread index (16^10 threads)
 
-// thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0 via the jump
-// polynomials x^(B*2^i) mod P for the set bits of t; output staged through a
-// 32x32 smem tile per warp so stores are coalesced rows.
+// state <- (poly)(T) state: 256 generator steps, the xor of the states at the
+// poly's set coefficients (branch-free, so lanes with different polys stay
+// converged)
+__device__ __forceinline__ void xo_apply(const unsigned long long* __restrict__ poly,
+                                         uint64_t s[4]) {
+  uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll 1
+  for (int w = 0; w < 4; ++w) {
+    uint64_t bits = __ldg(poly + w);
+#pragma unroll 8
+    for (int b = 0; b < 64; ++b) {
+      const uint64_t m = 0ull - (bits & 1);
+      acc[0] ^= s[0] & m;
+      acc[1] ^= s[1] & m;
+      acc[2] ^= s[2] & m;
+      acc[3] ^= s[3] & m;
+      bits >>= 1;
+      xo_step(s);
+    }
+  }
+  s[0] = acc[0];
+  s[1] = acc[1];
+  s[2] = acc[2];
+  s[3] = acc[3];
+}
+
+// thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0, one jump
+// polynomial x^(d*16^r*B) per nonzero base-16 digit d of t; output staged
+// through a 32x32 smem tile per warp so stores are coalesced rows.
 __global__ void __launch_bounds__(128)
     words_xoshiro(ulonglong4 s0, const uint64_t* __restrict__ polys, uint64_t n,
                   uint64_t* __restrict__ out) {
@@ -371,23 +483,10 @@ __global__ void __launch_bounds__(128)
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
-  for (int lvl = 0; lvl < kXoLevels; ++lvl) {
-    if (!((t >> lvl) & 1)) continue;
-    uint64_t acc[4] = {0, 0, 0, 0};
-    for (int b = 0; b < 256; ++b) {
-      if ((__ldg(reinterpret_cast<const unsigned long long*>(polys) + lvl * 4 + (b >> 6)) >>
-           (b & 63)) & 1) {
-        acc[0] ^= s[0];
-        acc[1] ^= s[1];
-        acc[2] ^= s[2];
-        acc[3] ^= s[3];
-      }
-      xo_step(s);
-    }
-    s[0] = acc[0];
-    s[1] = acc[1];
-    s[2] = acc[2];
-    s[3] = acc[3];
+  const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(polys);
+  for (int r = 0; r < kXoLevels && (t >> (4 * r)) != 0; ++r) {
+    const int d = (int)((t >> (4 * r)) & 15);
+    if (d) xo_apply(pp + ((size_t)r * 15 + d - 1) * 4, s);
   }
   const uint64_t warp_first = t - lane;  // thread index of lane 0
   for (int c = 0; c < kXoBlock; c += 32) {
@@ -507,7 +606,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   dbg("rp_count_starts", s);
   scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt2, boff2, nb, 0u, nullptr);
   EmitArgs a{interior, boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
-             scal + 3, scal + 2};
+             counters ? scal + 3 : nullptr, scal + 2};
   rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
   dbg("OutT>", s);
   ZF_TRY(cudaGetLastError());
@@ -594,10 +693,13 @@ int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cuda
   }
   if (gid != ZF_GEN_XOSHIRO256PP) return ZF_EDIST;
   const uint64_t threads = (n + kXoBlock - 1) / kXoBlock;
-  int levels = 0;
-  while (levels < kXoLevels && (threads - 1) >> levels) ++levels;
-  std::vector<uint64_t> polys((size_t)kXoLevels * 4, 0);
-  xoshiro_jump_polys(kXoBlock, std::max(levels, 1), polys.data());
+  if (threads - 1 >= (1ull << (4 * kXoLevels))) return ZF_ERANGE;
+  // the radix-16 table for B = kXoBlock never changes: build it once
+  static std::vector<uint64_t> polys = [] {
+    std::vector<uint64_t> p((size_t)kXoLevels * 15 * 4, 0);
+    xoshiro_radix16_polys(kXoBlock, kXoLevels, p.data());
+    return p;
+  }();
   uint64_t* dpolys = nullptr;
   ZF_TRY(cudaMallocAsync(&dpolys, polys.size() * sizeof(uint64_t), s));
   cudaError_t e = cudaMemcpyAsync(dpolys, polys.data(), polys.size() * sizeof(uint64_t),
