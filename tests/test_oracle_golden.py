@@ -134,3 +134,18 @@ def test_sharded_baseline_is_reference_sharding(orc):
         want = orc.fill_stream("exp", share, seed=orc.derive_seed(5, i))[0]
         assert np.array_equal(bits(out[off:off + share]), bits(want))
         off += share
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_sharded_fast_fill_equals_reference_fill(orc, dist):
+    """The CPU baseline's register-resident fast fill (orc_fill_sharded) gives
+    the same values as the general restatement, shard by shard
+    (quality.py:121-126 sharding: shard i seeded derive_seed(seed, i))."""
+    n, threads, seed = 300_001, 3, 1234
+    got = orc.fill_sharded(dist, n, seed, threads=threads)
+    off = 0
+    for i in range(threads):
+        share = n // threads + (1 if i < n % threads else 0)
+        want, _, _, _ = orc.fill_stream(dist, share, seed=orc.derive_seed(seed, i))
+        assert_bits_equal(got[off:off + share], bits(want), f"shard {i}")
+        off += share
