@@ -21,7 +21,10 @@
 // If the window is too short for n draws, the host doubles L and reruns.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
+#include <type_traits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -80,11 +83,11 @@ __device__ __forceinline__ T block_exclusive(T v, T identity, Op op, T* smem_war
 
 struct Add {
   template <typename T>
-  __device__ T operator()(T a, T b) const { return a + b; }
+  __host__ __device__ T operator()(T a, T b) const { return a + b; }
 };
 struct Max {
   template <typename T>
-  __device__ T operator()(T a, T b) const { return a > b ? a : b; }
+  __host__ __device__ T operator()(T a, T b) const { return a > b ? a : b; }
 };
 
 // ---- warp-striped position layout --------------------------------------------
@@ -153,27 +156,6 @@ __device__ __forceinline__ uint32_t warp_base(uint32_t warp_total, uint32_t* sme
   if (block_total) *block_total = tot;
   __syncthreads();
   return base;
-}
-
-// single-block exclusive scan over `cnt` entries (1024 threads)
-template <typename T, class Op>
-__global__ void scan_single(const T* __restrict__ in, T* __restrict__ out, uint64_t cnt,
-                            T identity, T* __restrict__ total) {
-  __shared__ T warp_buf[32];
-  const uint64_t chunk = (cnt + blockDim.x - 1) / blockDim.x;
-  const uint64_t beg = std::min<uint64_t>(threadIdx.x * chunk, cnt);
-  const uint64_t end = std::min<uint64_t>(beg + chunk, cnt);
-  Op op;
-  T local = identity;
-  for (uint64_t i = beg; i < end; ++i) local = op(local, in[i]);
-  T tot;
-  T run = block_exclusive<T>(local, identity, op, warp_buf, &tot);
-  for (uint64_t i = beg; i < end; ++i) {
-    const T x = in[i];
-    out[i] = run;
-    run = op(run, x);
-  }
-  if (threadIdx.x == 0 && total) *total = tot;
 }
 
 // ---- A: classify / compact ---------------------------------------------------
@@ -536,6 +518,28 @@ struct Workspace {
   }
 };
 
+// exclusive device scan (CUB) of n entries; *total (device, nullable) gets the
+// reduction of all n (= out[n-1] op in[n-1])
+template <typename T>
+__global__ void scan_total(const T* __restrict__ in, const T* __restrict__ out, uint64_t n,
+                           bool max_op, T* __restrict__ total) {
+  const T a = out[n - 1], b = in[n - 1];
+  *total = max_op ? (a > b ? a : b) : a + b;
+}
+
+template <typename T, class Op>
+int device_scan(Workspace& ws, const T* in, T* out, uint64_t n, Op op, T init, T* total,
+                cudaStream_t s) {
+  if (n == 0) return ZF_OK;
+  size_t bytes = 0;
+  ZF_TRY(cub::DeviceScan::ExclusiveScan(nullptr, bytes, in, out, op, init, (int64_t)n, s));
+  unsigned char* tmp = nullptr;
+  ZF_TRY(ws.alloc(&tmp, bytes));
+  ZF_TRY(cub::DeviceScan::ExclusiveScan(tmp, bytes, in, out, op, init, (int64_t)n, s));
+  if (total) scan_total<T><<<1, 1, 0, s>>>(in, out, n, std::is_same<Op, Max>::value, total);
+  return cuda_status(cudaGetLastError());
+}
+
 template <int DIST, typename OutT>
 int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, zf_path_rec* recs,
                   int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s) {
@@ -561,8 +565,8 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
   rp_count_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, bcnt);
   dbg("rp_count_exc", s);
-  scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt, boff, nb, 0u,
-                                                reinterpret_cast<uint32_t*>(scal));
+  ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt, boff, nb, Add(), 0u,
+                                      reinterpret_cast<uint32_t*>(scal), s));
   dbg("scan_exc", s);
   uint32_t m = 0;
   ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -591,7 +595,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   dbg("rp_draw_exc<DIST>", s);
     rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, m, bmax);
   dbg("rp_reach_max", s);
-    scan_single<uint64_t, Max><<<1, 1024, 0, s>>>(bmax, bpre, nbE, 0ull, nullptr);
+    ZF_TRY_STATUS(device_scan<uint64_t>(ws, bmax, bpre, nbE, Max(), 0ull, nullptr, s));
     rp_heads<<<nbE, kRT, 0, s>>>(E, eo.len, m, bpre, head);
   dbg("rp_heads", s);
     ZF_TRY(cudaMemsetAsync(real, 0, m, s));
@@ -604,7 +608,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   dbg("rp_mark", s);
   rp_count_starts<<<nb, kRT, 0, s>>>(interior, L, bcnt2);
   dbg("rp_count_starts", s);
-  scan_single<uint32_t, Add><<<1, 1024, 0, s>>>(bcnt2, boff2, nb, 0u, nullptr);
+  ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt2, boff2, nb, Add(), 0u, nullptr, s));
   EmitArgs a{interior, boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
              counters ? scal + 3 : nullptr, scal + 2};
   rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
