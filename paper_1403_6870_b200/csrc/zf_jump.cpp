@@ -6,7 +6,7 @@
 // set coefficients of the degree-<256 polynomial x^k mod P -- the same
 // "jump polynomial" scheme as the generator's published jump() routine, for
 // an arbitrary k.  P is recovered once by Berlekamp-Massey from a state-bit
-// sequence; the device kernel (zf_replay.cu) applies x^(B*2^i) mod P
+// sequence; the device kernel (zf_replay.cu) applies x^(d*16^r*B) mod P
 // polynomials to give every thread the start of its own block of the stream.
 #include <cstdint>
 #include <cstring>
@@ -140,15 +140,6 @@ void xoshiro_jump_host(uint64_t st[4], uint64_t k) {
     return;
   }
   apply(xpow(k), st);
-}
-
-void xoshiro_jump_polys(uint64_t block_words, int levels, uint64_t* out) {
-  std::call_once(g_once, compute_charpoly);
-  Poly p = xpow(block_words);
-  for (int i = 0; i < levels; ++i) {
-    std::memcpy(out + 4 * i, p.w, sizeof p.w);
-    p = mulmod(p, p);
-  }
 }
 
 // Radix-16 jump table: out[(r * 15 + d - 1) * 4 .. +4) = x^(d * 16^r * B) mod P

@@ -36,7 +36,10 @@ namespace zf {
 namespace {
 
 constexpr int kRT = 256;              // threads per block
-constexpr int kRI = 8;                // items per thread
+#ifndef ZF_RI
+#define ZF_RI 8
+#endif
+constexpr int kRI = ZF_RI;            // items per thread
 constexpr int kRB = kRT * kRI;        // positions per block
 constexpr uint32_t kIncomplete = 0xFFFFFFFFu;
 
