@@ -24,6 +24,7 @@ import math
 import numpy as np
 
 from . import _lib
+from .errors import ZigfastError
 from .tables import (EXPONENTIAL, HALF_NORMAL, ZigguratTables, build_alias, default_tables)
 from .uniform import CTR_LIMIT, UniformSource
 
@@ -185,8 +186,62 @@ class _SamplerBase:
         copy_stream.synchronize()
 
     # -- reference API -------------------------------------------------------------
+    _SAMPLE_BLOCK = 4096
+
     def sample(self) -> float:
-        return float(self._fill(1, False).item())
+        """One draw.  Production sources serve scalar draws from a block of
+        the next ``_SAMPLE_BLOCK`` values of their counter stream (one launch and
+        one copy per block); the source still advances by exactly one sample per
+        call, so interleaved fill() / sample() calls see the same stream as
+        repeated sample() calls.  Sequential (oracle-mode) sources draw one
+        sample per call, advancing the reference's state exactly."""
+        src = self.source
+        if src.gid != _lib.GEN_CTR:
+            return self._sample_sequential(src)
+        seed, ctr = int(src.state[0]), int(src.state[1])
+        cache = getattr(self, "_scalar_cache", None)
+        if cache is None or cache[0] != seed or not cache[1] <= ctr < cache[1] + len(cache[2]):
+            m = min(self._SAMPLE_BLOCK, CTR_LIMIT - ctr)
+            if m <= 0:
+                raise ValueError("counter stream exhausted (2^44 samples per seed)")
+            self.source = UniformSource.counter(seed, ctr)  # a throwaway copy
+            try:
+                cache = (seed, ctr, self._fill(m, False).cpu().numpy())
+            finally:
+                self.source = src
+            self._scalar_cache = cache
+        src.state[1] = np.uint64(ctr + 1)
+        return float(cache[2][ctr - cache[1]])
+
+    def _sample_sequential(self, src) -> float:
+        """Scalar draw from a sequential (reference) stream.  A block of the next
+        ``_SAMPLE_BLOCK`` draws and their word counts is resolved once on a
+        clone of the source; each call then returns the next value and advances
+        the real source by exactly that draw's words, as the reference's
+        `sample()` does.  Any outside change of the source state invalidates
+        the block; a block that cannot be resolved (a replay list on which some
+        later draw never finishes) falls back to one draw per call."""
+        k = 4 if src.gid == _lib.GEN_XOSHIRO else 1
+        c = getattr(self, "_seq_cache", None)
+        valid = (c is not None and c["src"] is src and c["state"] is src.state
+                 and c["i"] < len(c["vals"]) and np.array_equal(c["expect"], src.state[:k]))
+        if not valid:
+            probe = src.clone()
+            self.source = probe
+            try:
+                vals, recs = self.fill_records(self._SAMPLE_BLOCK)
+            except ZigfastError:
+                return float(self._fill(1, False).item())
+            finally:
+                self.source = src
+            c = {"src": src, "state": src.state, "vals": vals.cpu().numpy(),
+                 "nw": recs["nwords"].astype(np.int64), "i": 0}
+            self._seq_cache = c
+        i = c["i"]
+        src.jump(int(c["nw"][i]))
+        c["i"] = i + 1
+        c["expect"] = src.state[:k].copy()
+        return float(c["vals"][i])
 
     def sample_counted(self) -> float:
         return float(self._fill(1, True).item())

@@ -169,3 +169,24 @@ def test_cycling_replay_is_an_error_not_a_hang(zf, cuda):
     with pytest.raises(DeviceError) as ei:
         s.fill(100)
     assert ei.value.status == -4
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_scalar_samples_interleave_with_fills(zf, orc, cuda, dist):
+    """sample() on a reference stream serves a cached block of draws but
+    advances the source by exactly each draw's words: interleaving sample()
+    and fill() equals one fill, with the reference's state at every point."""
+    want, _, _, _ = orc.fill_stream(dist, 6000, seed=5)
+    s = cls_of(zf, dist)(source=zf.UniformSource(5), device=cuda)
+    got = [s.sample() for _ in range(10)]
+    got += list(s.fill(500).cpu().numpy())
+    got += [s.sample() for _ in range(4200)]  # crosses a cached block
+    got += list(s.fill(3).cpu().numpy())
+    assert np.array_equal(bits(np.array(got)), bits(want[:len(got)]))
+    ref = zf.UniformSource(5)
+    _, _, _, used = orc.fill_stream(dist, len(got), seed=5)
+    ref.jump(used)
+    assert np.array_equal(s.source.state, ref.state)
+    # an outside reseed invalidates the cached block
+    s.source.state[:] = zf.UniformSource(5).state
+    assert bits(np.array([s.sample()]))[0] == bits(want[:1])[0]

@@ -204,3 +204,20 @@ def test_concurrent_host_threads(zf, orc, cuda):
     for i in range(6):
         want, _, _ = orc.fill_ctr("normal" if i % 2 else "exp", 200_000, seed=100 + i)
         assert np.array_equal(bits(results[i]), bits(want)), i
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_scalar_samples_interleave_with_fills(zf, cuda, dist):
+    """sample() serves production draws from a cached block but advances the
+    stream by one per call: any interleaving of sample() and fill() equals one
+    long fill, and an external counter change invalidates the block."""
+    whole = sampler(zf, dist, 31, device=cuda).fill(9000).cpu().numpy()
+    s = sampler(zf, dist, 31, device=cuda)
+    got = [s.sample() for _ in range(3)]
+    got += list(s.fill(100).cpu().numpy())
+    got += [s.sample() for _ in range(5000)]  # crosses a cache block
+    got += list(s.fill(7).cpu().numpy())
+    got += [s.sample() for _ in range(2)]
+    assert np.array_equal(bits(np.array(got)), bits(whole[:len(got)]))
+    s.source.state[1] = np.uint64(5)  # rewind: the cached block must not be reused blindly
+    assert bits(np.array([s.sample()]))[0] == bits(whole[5:6])[0]
