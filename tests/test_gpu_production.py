@@ -221,3 +221,17 @@ def test_scalar_samples_interleave_with_fills(zf, cuda, dist):
     assert np.array_equal(bits(np.array(got)), bits(whole[:len(got)]))
     s.source.state[1] = np.uint64(5)  # rewind: the cached block must not be reused blindly
     assert bits(np.array([s.sample()]))[0] == bits(whole[5:6])[0]
+
+
+def test_batch_fp32_and_counter_bases(zf, orc, cuda):
+    """fp32 batches (4-element alignment padding) and nonzero counter bases."""
+    import torch
+    dists = ["exp", "normal", "normal", "exp", "exp"]
+    ns = [1, 511, 4097, 20000, 3]
+    seeds = [5, 6, 7, 8, 9]
+    bases = [0, 1 << 40, 123, (1 << 44) - 30000, 77]
+    plan = zf.BatchPlan(dists, ns, seeds, bases, dtype="float32")
+    out = plan.fill(device=cuda).cpu().numpy()
+    for d, n, sd, b, off in zip(dists, ns, seeds, bases, plan.offsets):
+        want, _, _ = orc.fill_ctr(d, n, seed=sd, ctr_base=b)
+        assert np.array_equal(out[off:off + n], want.astype(np.float32)), (d, n, sd, b)
