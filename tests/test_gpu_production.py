@@ -235,3 +235,16 @@ def test_batch_fp32_and_counter_bases(zf, orc, cuda):
     for d, n, sd, b, off in zip(dists, ns, seeds, bases, plan.offsets):
         want, _, _ = orc.fill_ctr(d, n, seed=sd, ctr_base=b)
         assert np.array_equal(out[off:off + n], want.astype(np.float32)), (d, n, sd, b)
+
+
+@pytest.mark.parametrize("dist", DISTS)
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_misaligned_fp32_views(zf, orc, cuda, dist, shift):
+    """fp32 outputs 4-byte aligned but not 16: the scalar-store kernel variant."""
+    import torch
+    buf = torch.zeros(5003, dtype=torch.float32, device=cuda)
+    view = buf[shift:shift + 4000]
+    sampler(zf, dist, 13, device=cuda).fill(view)
+    want, _, _ = orc.fill_ctr(dist, 4000, seed=13)
+    assert np.array_equal(view.cpu().numpy(), want.astype(np.float32))
+    assert buf[:shift].abs().sum().item() == 0.0 and buf[shift + 4000:].abs().sum().item() == 0.0
