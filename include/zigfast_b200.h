@@ -147,6 +147,12 @@ int zf_tables_create(const zf_table_pack* exp_pack, const zf_table_pack* halfnor
  * replaces the per-sampler `_pack` of _TraditionalSampler (traditional.py:124-135). */
 int zf_trad_tables_create(const zf_trad_pack* exp_pack, const zf_trad_pack* hn_pack, int device,
                           zf_tables** out);
+/* The reference's default tables (default_tables("exponential" /
+ * "halfnormal") + make_alias, tables.py:359-372, _packs.py:31-64), or the
+ * solved traditional tables (solve_traditional(kind, 256), traditional.py:56-96),
+ * embedded in the library: no host-side table code needed. */
+int zf_tables_create_default(int device, zf_tables** out);
+int zf_trad_tables_create_default(int device, zf_tables** out);
 int zf_tables_destroy(zf_tables* t);
 
 /* Production mode: sample k (0 <= k < n) of the call is global sample

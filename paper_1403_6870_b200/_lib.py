@@ -30,7 +30,8 @@ EXPORTS = (
     "zf_abi_version", "zf_strerror", "zf_tables_create", "zf_tables_destroy", "zf_fill",
     "zf_fill_stats", "zf_stats", "zf_stats_blocks", "zf_fill_replay", "zf_fill_gid", "zf_words",
     "zf_xoshiro_jump", "zf_xoshiro_pow2_poly", "zf_fill_batch", "zf_trad_tables_create",
-    "zf_format_g17", "zf_format_scratch_words",
+    "zf_format_g17", "zf_format_scratch_words", "zf_tables_create_default",
+    "zf_trad_tables_create_default",
 )
 EXP, NORMAL, TRAD_EXP, TRAD_NORMAL = 0, 1, 2, 3
 
@@ -100,6 +101,8 @@ def lib():
                                                 C.POINTER(vp)]),
                 "zf_format_g17": (i32, [vp, u64, vp, u64, vp, vp]),
                 "zf_format_scratch_words": (u64, [u64]),
+                "zf_tables_create_default": (i32, [i32, C.POINTER(vp)]),
+                "zf_trad_tables_create_default": (i32, [i32, C.POINTER(vp)]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <new>
 
+#include "zf_default_tables.h"
 #include "zf_internal.h"
 
 namespace zf {
@@ -167,6 +168,26 @@ int zf_trad_tables_create(const zf_trad_pack* exp_pack, const zf_trad_pack* hn_p
   }
   *out = t;
   return ZF_OK;
+}
+
+// The reference's default tables, packed at build time (build/gen, see
+// _build.generate_default_tables): a non-Python host (cgo, JNI, C) gets the
+// drop-in samplers without any table code of its own.
+int zf_tables_create_default(int device, zf_tables** out) {
+  const zf_table_pack e{kDef_exp_lmax, kDef_exp_lmax + 1, kDef_exp_scale, kDef_exp_xlo,
+                        kDef_exp_xw,   kDef_exp_flo,      kDef_exp_fh,    kDef_exp_eps,
+                        kDef_exp_prob, kDef_exp_alias,    kDef_exp_tailx};
+  const zf_table_pack h{kDef_hn_lmax, kDef_hn_lmax + 1, kDef_hn_scale, kDef_hn_xlo,
+                        kDef_hn_xw,   kDef_hn_flo,      kDef_hn_fh,    kDef_hn_eps,
+                        kDef_hn_prob, kDef_hn_alias,    kDef_hn_tailx};
+  return zf_tables_create(&e, &h, device, out);
+}
+
+int zf_trad_tables_create_default(int device, zf_tables** out) {
+  const zf_trad_pack e{256, kDef_texp_se, kDef_texp_kk, kDef_texp_flo, kDef_texp_fh,
+                       kDef_texp_r};
+  const zf_trad_pack h{256, kDef_thn_se, kDef_thn_kk, kDef_thn_flo, kDef_thn_fh, kDef_thn_r};
+  return zf_trad_tables_create(&e, &h, device, out);
 }
 
 int zf_tables_destroy(zf_tables* t) {
