@@ -17,6 +17,7 @@ import threading
 from .errors import (BitBudgetExceeded, DeviceError, EmptyWeights, ExtensionMissing,
                      FormatError, NonConvergence, ZigfastError)
 from .batch import BatchPlan, fill_batch
+from .construct import build_tables, verify_tables
 from .quality import EXPECTED_MOMENTS, QualityReport, run_quality
 from .samplers import ExpSampler, NormalSampler, PathCounts
 from .tables import (EXPONENTIAL, HALF_NORMAL, AliasTable, ZigguratTables, build_alias,
@@ -59,7 +60,7 @@ def normal(size: int, device=None):
 
 
 __all__ = [
-    "AliasTable", "BatchPlan", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
+    "AliasTable", "BatchPlan", "build_tables", "verify_tables", "BitBudgetExceeded", "DeviceError", "EXPECTED_MOMENTS", "EXPONENTIAL",
     "EmptyWeights", "ExpSampler", "ExtensionMissing", "FormatError", "HALF_NORMAL",
     "NonConvergence", "NormalSampler", "PathCounts", "QualityReport",
     "TraditionalExpSampler", "TraditionalNormalSampler", "TraditionalTables", "UniformSource",
