@@ -284,16 +284,25 @@ int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* stat
   // exactly the words consumed.  Grow the window if it was too short.
   uint64_t L = n + n / 8 + 4096;
   for (int attempt = 0; attempt < 8; ++attempt, L *= 2) {
-    uint64_t* words = nullptr;
-    ZF_TRY(cudaMallocAsync(&words, L * sizeof(uint64_t), s));
-    uint64_t st[4] = {state[0], gid == ZF_GEN_XOSHIRO256PP ? state[1] : 0,
-                      gid == ZF_GEN_XOSHIRO256PP ? state[2] : 0,
-                      gid == ZF_GEN_XOSHIRO256PP ? state[3] : 0};
-    int rc = launch_words(gid, st, L, words, s);
-    if (rc == ZF_OK)
-      rc = run_replay(t, dist, dtype, words, L, 0, 0, out_dev, n, recs_dev, counters_dev,
-                      &consumed, s);
-    cudaFreeAsync(words, s);
+    const uint64_t st[4] = {state[0], gid == ZF_GEN_XOSHIRO256PP ? state[1] : 0,
+                            gid == ZF_GEN_XOSHIRO256PP ? state[2] : 0,
+                            gid == ZF_GEN_XOSHIRO256PP ? state[3] : 0};
+    int rc;
+    if (L >= (1ull << 22)) {
+      // large windows: classify while generating (saves two passes over the
+      // window); small ones keep more threads busy in the separate passes
+      rc = run_generated(t, dist, dtype, gid, st, L, out_dev, n, recs_dev, counters_dev,
+                         &consumed, s);
+    } else {
+      uint64_t* words = nullptr;
+      ZF_TRY(cudaMallocAsync(&words, L * sizeof(uint64_t), s));
+      uint64_t st2[4] = {st[0], st[1], st[2], st[3]};
+      rc = launch_words(gid, st2, L, words, s);
+      if (rc == ZF_OK)
+        rc = run_replay(t, dist, dtype, words, L, 0, 0, out_dev, n, recs_dev, counters_dev,
+                        &consumed, s);
+      cudaFreeAsync(words, s);
+    }
     if (rc == ZF_ESHORT) continue;
     ZF_TRY_STATUS(rc);
     if (gid == ZF_GEN_XOSHIRO256PP) xoshiro_jump_host(state, consumed);

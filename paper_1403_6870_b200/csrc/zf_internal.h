@@ -58,6 +58,11 @@ int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, u
                uint64_t cursor, int wrap, void* out, uint64_t n, zf_path_rec* recs,
                int64_t* counters, uint64_t* consumed, cudaStream_t s);
 int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cudaStream_t s);
+// one oracle-mode window of L words generated from state (gid 0/1) and
+// classified in the same pass; ZF_ESHORT when L was too short for n samples
+int run_generated(const zf_tables* t, int dist, int dtype, int gid, const uint64_t st[4],
+                  uint64_t L, void* out, uint64_t n, zf_path_rec* recs, int64_t* counters,
+                  uint64_t* consumed, cudaStream_t s);
 // launchers (zf_format.cu)
 uint64_t format_blocks(uint64_t n);
 int launch_format_g17(const double* x, uint64_t n, char* out, uint64_t cap, uint64_t* scratch,

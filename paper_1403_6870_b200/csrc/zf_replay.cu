@@ -326,6 +326,7 @@ struct EmitArgs {
   zf_path_rec* recs;
   unsigned long long* counters;  // internal [6]
   unsigned long long* consumed;  // internal scalar
+  uint32_t boff_stride;          // boff_exc entries per emit block (1, or 2 with segments)
 };
 
 template <int DIST, typename OutT>
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kRT)
   }
   uint32_t eidx, rank;
   warp_base2(ce, cs, wb, &eidx, &rank);
-  eidx += a.boff_exc[blockIdx.x];
+  eidx += a.boff_exc[(uint64_t)blockIdx.x * a.boff_stride];
   rank += a.boff_start[blockIdx.x];
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -489,6 +490,95 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---- generated windows: words + classification in one pass ----------------------
+// For the reference's own generators (gid 0/1) the window is produced on the
+// device anyway; the kernel that writes it also flags the exceptional words of
+// each thread's 1024-word segment into per-segment slots, so the replay
+// pipeline skips its two classification passes over the window.
+
+struct XoGen {
+  uint64_t s[4];
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t r = ((s[0] + s[3]) << 23 | (s[0] + s[3]) >> 41) + s[0];
+    xo_step(s);
+    return r;
+  }
+};
+struct SmGen {
+  uint64_t st;
+  __device__ __forceinline__ uint64_t next() {
+    st += kGamma;
+    return mix13(st);
+  }
+};
+
+constexpr int kClsCap = 64;  // exceptional slots per segment (expected ~16)
+static_assert(kRB % kXoBlock == 0, "emit blocks cover whole segments");
+
+template <int DIST, int GID>
+__global__ void __launch_bounds__(128)
+    words_cls(ulonglong4 s0, const uint64_t* __restrict__ polys, uint64_t n,
+              uint64_t* __restrict__ out, const DevPack* __restrict__ P,
+              uint32_t* __restrict__ slots, uint32_t* __restrict__ slot_cnt,
+              unsigned int* __restrict__ overflow) {
+  __shared__ uint64_t tile[4][32][33];
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  using G = typename std::conditional<GID == ZF_GEN_XOSHIRO256PP, XoGen, SmGen>::type;
+  G g;
+  if constexpr (GID == ZF_GEN_XOSHIRO256PP) {
+    g = XoGen{{s0.x, s0.y, s0.z, s0.w}};
+    const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(polys);
+    for (int r = 0; r < kXoLevels && (t >> (4 * r)) != 0; ++r) {
+      const int d = (int)((t >> (4 * r)) & 15);
+      if (d) xo_apply(pp + ((size_t)r * 15 + d - 1) * 4, g.s);
+    }
+  } else {
+    g = SmGen{s0.x + t * (uint64_t)kXoBlock * kGamma};
+  }
+  const uint64_t warp_first = t - lane;
+  const uint64_t p0 = t * kXoBlock;
+  uint32_t k = 0;
+  for (int c = 0; c < kXoBlock; c += 32) {
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const uint64_t w = g.next();
+      tile[wid][lane][j] = w;
+      const uint64_t p = p0 + c + j;
+      if (p < n && exc_word<DIST>(*P, w)) {
+        if (k < kClsCap) slots[t * kClsCap + k] = (uint32_t)p;
+        ++k;
+      }
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {
+      const uint64_t idx = (warp_first + r) * kXoBlock + c + lane;
+      if (idx < n) out[idx] = tile[wid][r][lane];
+    }
+    __syncwarp();
+  }
+  if (p0 < n) {
+    slot_cnt[t] = k < kClsCap ? k : kClsCap;
+    if (k > kClsCap) atomicOr(overflow, 1u);
+  }
+}
+
+__global__ void cls_compact(const uint32_t* __restrict__ slot_cnt, const uint32_t* __restrict__ coff,
+                            uint64_t T, const uint32_t* __restrict__ slots,
+                            uint32_t* __restrict__ E) {
+  const uint64_t slot = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t t = slot / kClsCap, k = slot % kClsCap;
+  if (t < T && k < slot_cnt[t]) E[coff[t] + k] = slots[slot];
+}
+
+// pre-classified window (words_cls): slots per segment + overflow flag
+struct PreClass {
+  const uint32_t* slots;
+  const uint32_t* slot_cnt;
+  uint64_t T;
+  const unsigned int* overflow;
+};
+
 // ZF_DEBUG=1: synchronise and report after every pipeline stage (stderr)
 static bool debug_on() {
   static const bool on = getenv("ZF_DEBUG") != nullptr;
@@ -545,7 +635,8 @@ int device_scan(Workspace& ws, const T* in, T* out, uint64_t n, Op op, T init, T
 
 template <int DIST, typename OutT>
 int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, zf_path_rec* recs,
-                  int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s) {
+                  int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s,
+                  const PreClass* pre = nullptr) {
   *retry = false;
   if (debug_on()) fprintf(stderr, "[zf] replay_window L=%llu nwords=%llu cursor=%llu n=%llu\n",
                           (unsigned long long)win.L, (unsigned long long)win.nwords,
@@ -566,14 +657,31 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   if (debug_on()) fprintf(stderr, "[zf] workspace allocated\n");
   ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
   ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
-  rp_count_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, bcnt);
-  dbg("rp_count_exc", s);
-  ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt, boff, nb, Add(), 0u,
-                                      reinterpret_cast<uint32_t*>(scal), s));
-  dbg("scan_exc", s);
+  // exceptional positions: from the generator's slots, or two passes here
+  uint32_t* coff = nullptr;
+  uint32_t boff_stride = 1;
   uint32_t m = 0;
-  ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  ZF_TRY(cudaStreamSynchronize(s));
+  bool use_pre = pre != nullptr;
+  if (use_pre) {
+    ZF_TRY(ws.alloc(&coff, pre->T));
+    ZF_TRY_STATUS(device_scan<uint32_t>(ws, pre->slot_cnt, coff, pre->T, Add(), 0u,
+                                        reinterpret_cast<uint32_t*>(scal), s));
+    unsigned int ovf = 0;
+    ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ZF_TRY(cudaMemcpyAsync(&ovf, pre->overflow, sizeof ovf, cudaMemcpyDeviceToHost, s));
+    ZF_TRY(cudaStreamSynchronize(s));
+    if (ovf) use_pre = false;  // some segment overflowed its slots: classify here
+    else boff_stride = (uint32_t)(kRB / kXoBlock);
+  }
+  if (!use_pre) {
+    rp_count_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, bcnt);
+    dbg("rp_count_exc", s);
+    ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt, boff, nb, Add(), 0u,
+                                        reinterpret_cast<uint32_t*>(scal), s));
+    dbg("scan_exc", s);
+    ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ZF_TRY(cudaStreamSynchronize(s));
+  }
   ExcOut eo;
   uint8_t *head, *real;
   uint64_t *bmax, *bpre;
@@ -587,8 +695,14 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(ws.alloc(&real, m));
   ZF_TRY(ws.alloc(&bmax, nbE));
   ZF_TRY(ws.alloc(&bpre, nbE));
-  rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E);
-  dbg("rp_compact_exc", s);
+  if (use_pre) {
+    const uint64_t slots = pre->T * kClsCap;
+    cls_compact<<<(uint32_t)((slots + 255) / 256), 256, 0, s>>>(pre->slot_cnt, coff, pre->T,
+                                                                pre->slots, E);
+  } else {
+    rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E);
+  }
+  dbg("compact", s);
   if (m) {
     constexpr int kPacks = kPacksOf<DIST>;
     const size_t smem = kPacks * sizeof(DevPack);
@@ -612,8 +726,8 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   rp_count_starts<<<nb, kRT, 0, s>>>(interior, L, bcnt2);
   dbg("rp_count_starts", s);
   ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt2, boff2, nb, Add(), 0u, nullptr, s));
-  EmitArgs a{interior, boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
-             counters ? scal + 3 : nullptr, scal + 2};
+  EmitArgs a{interior, use_pre ? coff : boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
+             counters ? scal + 3 : nullptr, scal + 2, boff_stride};
   rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
   dbg("OutT>", s);
   ZF_TRY(cudaGetLastError());
@@ -652,7 +766,74 @@ int replay_typed(const zf_tables* t, const uint64_t* words, uint64_t nwords, uin
   }
 }
 
+// one window of L generated words (gid 0/1), classified while generated
+template <int DIST, typename OutT>
+int generated_window(const zf_tables* t, int gid, const uint64_t st[4], uint64_t L, void* out,
+                     uint64_t n, zf_path_rec* recs, int64_t* counters, uint64_t* consumed,
+                     cudaStream_t s) {
+  Workspace ws(s);
+  const uint64_t T = (L + kXoBlock - 1) / kXoBlock;
+  uint64_t* words;
+  uint32_t *slots, *slot_cnt;
+  unsigned int* overflow;
+  ZF_TRY(ws.alloc(&words, L));
+  ZF_TRY(ws.alloc(&slots, T * kClsCap));
+  ZF_TRY(ws.alloc(&slot_cnt, T));
+  ZF_TRY(ws.alloc(&overflow, 1));
+  ZF_TRY(cudaMemsetAsync(overflow, 0, sizeof(unsigned int), s));
+  uint64_t* dpolys = nullptr;
+  if (gid == ZF_GEN_XOSHIRO256PP) {
+    if (T - 1 >= (1ull << (4 * kXoLevels))) return ZF_ERANGE;
+    static std::vector<uint64_t> polys = [] {
+      std::vector<uint64_t> p((size_t)kXoLevels * 15 * 4, 0);
+      xoshiro_radix16_polys(kXoBlock, kXoLevels, p.data());
+      return p;
+    }();
+    ZF_TRY(ws.alloc(&dpolys, polys.size()));
+    ZF_TRY(cudaMemcpyAsync(dpolys, polys.data(), polys.size() * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, s));
+  }
+  const ulonglong4 s0 = make_ulonglong4(st[0], st[1], st[2], st[3]);
+  const uint64_t blocks = (T + 127) / 128;
+  const DevPack* dP = primary_pack<DIST>(t->dev);
+  if (gid == ZF_GEN_XOSHIRO256PP)
+    words_cls<DIST, ZF_GEN_XOSHIRO256PP><<<(uint32_t)blocks, 128, 0, s>>>(
+        s0, dpolys, L, words, dP, slots, slot_cnt, overflow);
+  else
+    words_cls<DIST, ZF_GEN_SPLITMIX64><<<(uint32_t)blocks, 128, 0, s>>>(
+        s0, dpolys, L, words, dP, slots, slot_cnt, overflow);
+  ZF_TRY(cudaGetLastError());
+  Window win{words, L, 0, L};
+  PreClass pre{slots, slot_cnt, T, overflow};
+  bool retry = false;
+  ZF_TRY_STATUS((replay_window<DIST, OutT>(t, win, out, n, recs, counters, consumed, &retry, s,
+                                           &pre)));
+  return retry ? ZF_ESHORT : ZF_OK;
+}
+
 }  // namespace
+
+int run_generated(const zf_tables* t, int dist, int dtype, int gid, const uint64_t st[4],
+                  uint64_t L, void* out, uint64_t n, zf_path_rec* recs, int64_t* counters,
+                  uint64_t* consumed, cudaStream_t s) {
+  *consumed = 0;
+  if (n == 0) return ZF_OK;
+  if (!out) return ZF_EINVAL;
+  if (n >= (1ull << 31) || L >= (1ull << 32) - kRB) return ZF_ERANGE;
+  if (gid != ZF_GEN_XOSHIRO256PP && gid != ZF_GEN_SPLITMIX64) return ZF_EDIST;
+  ZF_TRY_STATUS(check_kind(t, dist));
+#define ZF_GEN(D, O) return generated_window<D, O>(t, gid, st, L, out, n, recs, counters, consumed, s)
+  if (dist == ZF_EXP && dtype == ZF_F64) ZF_GEN(ZF_EXP, double);
+  if (dist == ZF_EXP && dtype == ZF_F32) ZF_GEN(ZF_EXP, float);
+  if (dist == ZF_NORMAL && dtype == ZF_F64) ZF_GEN(ZF_NORMAL, double);
+  if (dist == ZF_NORMAL && dtype == ZF_F32) ZF_GEN(ZF_NORMAL, float);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F64) ZF_GEN(ZF_TRAD_EXP, double);
+  if (dist == ZF_TRAD_EXP && dtype == ZF_F32) ZF_GEN(ZF_TRAD_EXP, float);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F64) ZF_GEN(ZF_TRAD_NORMAL, double);
+  if (dist == ZF_TRAD_NORMAL && dtype == ZF_F32) ZF_GEN(ZF_TRAD_NORMAL, float);
+#undef ZF_GEN
+  return ZF_EDIST;
+}
 
 int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, uint64_t nwords,
                uint64_t cursor, int wrap, void* out, uint64_t n, zf_path_rec* recs,

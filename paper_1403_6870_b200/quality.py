@@ -60,10 +60,14 @@ def _cfg(hist=None, thresholds=(), abs_thresh=False, moments=5) -> _lib.StatsCfg
     return cfg
 
 
-def _collect(n, partials, counts, cfg, thresholds) -> StatsResult:
+def _collect(n, partials, counts, cfg, thresholds, moments: int = 5) -> StatsResult:
     p = partials.cpu().numpy().reshape(-1, 5)
-    c = counts.cpu().numpy().astype(np.int64)
-    sums = [math.fsum(p[:, k].tolist()) for k in range(5)]
+    c = counts.cpu().numpy().astype(np.int64) if (cfg.nbins or cfg.nthresh) else None
+    # exact merge of the per-block rows; unrequested moments are not summed
+    sums = [math.fsum(p[:, k].tolist()) if k < moments else math.nan for k in range(5)]
+    if c is None:
+        return StatsResult(n=n, sums=sums, hist=np.zeros(0, dtype=np.int64), thresh_counts=[],
+                           thresholds=list(thresholds))
     nb = cfg.nbins
     hist = c[:nb + 2] if nb else np.zeros(0, dtype=np.int64)
     # counts layout: [nbins + 2 histogram slots][thresholds] (2 unused slots if nbins == 0)
@@ -96,7 +100,7 @@ def device_sums(sampler, n: int, moments: int = 5, hist=None, thresholds=(), abs
             C.byref(cfg), partials.data_ptr(), counts.data_ptr(),
             _lib.stream_handle(sampler.device)))
     src.state[1] = np.uint64(int(src.state[1]) + n)
-    res = _collect(n, partials, counts, cfg, thresholds)
+    res = _collect(n, partials, counts, cfg, thresholds, moments)
     return res.sums[:moments], res
 
 
@@ -110,7 +114,7 @@ def buffer_sums(x, moments: int = 5, hist=None, thresholds=(), abs_thresh=False)
     with torch.cuda.device(x.device):
         _lib.check(_lib.lib().zf_stats(dtype, x.data_ptr(), n, C.byref(cfg), partials.data_ptr(),
                                        counts.data_ptr(), _lib.stream_handle(x.device)))
-    res = _collect(n, partials, counts, cfg, thresholds)
+    res = _collect(n, partials, counts, cfg, thresholds, moments)
     return res.sums[:moments], res
 
 

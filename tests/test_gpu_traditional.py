@@ -200,7 +200,7 @@ def test_run_bench_speedup(zf, cuda, dist, generator):
     >= 1.2x; on the reference's sequential stream the parallel resolution of
     the word stream dominates both, so only the harness itself is checked."""
     from paper_1403_6870_b200.bench import run_bench
-    n = 1 << 26 if generator == "ctr" else 1 << 22
+    n = 1 << 28 if generator == "ctr" else 1 << 22
     reps = run_bench(["modified", "traditional"], dist, n, trials=3, seed=1,
                      generator=generator, device=cuda)
     mod = {r.algorithm: r for r in reps}["modified"]
