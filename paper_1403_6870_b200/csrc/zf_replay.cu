@@ -286,32 +286,32 @@ __global__ void rp_walk(const uint32_t* __restrict__ E, const uint32_t* __restri
 }
 
 // ---- D: interior marks -----------------------------------------------------------
+// mark the interior words of every real draw, and count them per emit block
+// (real draws never overlap, so the counts are exact)
 __global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
                         const uint8_t* __restrict__ real, uint32_t m, uint64_t L,
-                        uint8_t* __restrict__ interior) {
+                        uint8_t* __restrict__ interior, uint32_t* __restrict__ block_int) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m || !real[i]) return;
   const uint64_t p = E[i];
   const uint64_t stop = len[i] == kIncomplete ? L : std::min<uint64_t>(p + len[i], L);
   for (uint64_t q = p + 1; q < stop; ++q) interior[q] = 1;
+  for (uint64_t q = p + 1; q < stop;) {
+    const uint64_t b = q / kRB, e = std::min<uint64_t>(stop, (b + 1) * kRB);
+    atomicAdd(block_int + b, (uint32_t)(e - q));
+    q = e;
+  }
 }
 
-__global__ void __launch_bounds__(kRT)
-    rp_count_starts(const uint8_t* __restrict__ interior, uint64_t L, uint32_t* __restrict__ bcnt) {
-  __shared__ uint32_t wb[kRT / 32];
-  uint8_t v[kRI];
-#pragma unroll
-  for (int j = 0; j < kRI; ++j) {
-    const uint64_t p = striped_pos(j);
-    v[j] = p < L ? interior[p] : 1;
-  }
-  uint32_t c = 0;
-#pragma unroll
-  for (int j = 0; j < kRI; ++j) c += __popc(__ballot_sync(0xffffffffu, v[j] == 0));
-  uint32_t tot;
-  warp_base(c, wb, &tot);
-  if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+// start positions per emit block = block length - interior words
+__global__ void rp_block_starts(const uint32_t* __restrict__ block_int, uint32_t nb, uint64_t L,
+                                uint32_t* __restrict__ starts) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t len = std::min<uint64_t>(L, (uint64_t)(b + 1) * kRB) - (uint64_t)b * kRB;
+  starts[b] = (uint32_t)(len - block_int[b]);
 }
+
 
 // ---- E: emit -------------------------------------------------------------------------
 struct EmitArgs {
@@ -721,10 +721,11 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   dbg("rp_walk", s);
   }
   ZF_TRY(cudaMemsetAsync(interior, 0, L, s));
-  if (m) rp_mark<<<(m + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, m, L, interior);
+  ZF_TRY(cudaMemsetAsync(bcnt, 0, nb * sizeof(uint32_t), s));  // reused: interior per block
+  if (m) rp_mark<<<(m + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, m, L, interior, bcnt);
   dbg("rp_mark", s);
-  rp_count_starts<<<nb, kRT, 0, s>>>(interior, L, bcnt2);
-  dbg("rp_count_starts", s);
+  rp_block_starts<<<(nb + 255) / 256, 256, 0, s>>>(bcnt, nb, L, bcnt2);
+  dbg("rp_block_starts", s);
   ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt2, boff2, nb, Add(), 0u, nullptr, s));
   EmitArgs a{interior, use_pre ? coff : boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
              counters ? scal + 3 : nullptr, scal + 2, boff_stride};
