@@ -116,8 +116,8 @@ __device__ __forceinline__ void load_striped(const Window& win, uint64_t w[kRI])
       const uint64_t p = striped_pos(j);
       w[j] = p < win.L ? __ldg(base + win.cursor + p) : 0;
     }
-  } else {
-#pragma unroll 1
+  } else {  // unrolled too: a dynamic index would put w[] in local memory
+#pragma unroll
     for (int j = 0; j < kRI; ++j) {
       const uint64_t p = striped_pos(j);
       w[j] = p < win.L ? win.word(p) : 0;
@@ -329,8 +329,11 @@ struct EmitArgs {
   uint32_t boff_stride;          // boff_exc entries per emit block (1, or 2 with segments)
 };
 
+#ifndef ZF_EMIT_MINB
+#define ZF_EMIT_MINB 6  // 40 registers: occupancy hides the load latency
+#endif
 template <int DIST, typename OutT>
-__global__ void __launch_bounds__(kRT)
+__global__ void __launch_bounds__(kRT, ZF_EMIT_MINB)
     rp_emit(const DevTables* __restrict__ gt, Window win, EmitArgs a, OutT* __restrict__ out) {
   __shared__ uint2 wb[kRT / 32];
   const DevPack* P = primary_pack<DIST>(gt);
