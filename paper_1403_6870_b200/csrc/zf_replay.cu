@@ -433,7 +433,10 @@ __device__ __forceinline__ void xo_step(uint64_t s[4]) {
   s[3] = (s[3] << 45) | (s[3] >> 19);
 }
 
-constexpr int kXoBlock = 1024;  // words per thread
+#ifndef ZF_XO_BLOCK
+#define ZF_XO_BLOCK 1024
+#endif
+constexpr int kXoBlock = ZF_XO_BLOCK;  // words per thread
 constexpr int kXoLevels = 10;   // radix-16 digits of the thread index (16^10 threads)
 
 // state <- (poly)(T) state: 256 generator steps, the xor of the states at the
