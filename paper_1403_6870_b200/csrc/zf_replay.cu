@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(128)
   }
   const uint64_t warp_first = t - lane;
   const uint64_t p0 = t * kXoBlock;
+  const uint32_t lmax = (uint32_t)__ldg(&P->lmax);  // hoisted: one load per thread
   uint32_t k = 0;
   for (int c = 0; c < kXoBlock; c += 32) {
 #pragma unroll 4
@@ -551,7 +552,8 @@ __global__ void __launch_bounds__(128)
       const uint64_t w = g.next();
       tile[wid][lane][j] = w;
       const uint64_t p = p0 + c + j;
-      if (p < n && exc_word<DIST>(*P, w)) {
+      const bool exc = kTrad<DIST> ? exc_word<DIST>(*P, w) : ((uint32_t)w & 0xFFu) >= lmax;
+      if (exc && p < n) {
         if (k < kClsCap) slots[t * kClsCap + k] = (uint32_t)p;
         ++k;
       }
