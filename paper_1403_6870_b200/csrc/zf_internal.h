@@ -69,7 +69,8 @@ int launch_format_g17(const double* x, uint64_t n, char* out, uint64_t cap, uint
                       cudaStream_t s);
 // xoshiro jump-ahead (zf_jump.cpp)
 void xoshiro_jump_host(uint64_t st[4], uint64_t k);
-// x^(d * 16^r * B) mod P for r < levels, d = 1..15: levels x 15 x 4 words
-void xoshiro_radix16_polys(uint64_t block_words, int levels, uint64_t* out);
+// x^(d * R^r * B) mod P for r < levels, d = 1..R-1, R = 2^bits:
+// levels x (R - 1) x 4 words
+void xoshiro_radix_polys(uint64_t block_words, int bits, int levels, uint64_t* out);
 
 }  // namespace zf

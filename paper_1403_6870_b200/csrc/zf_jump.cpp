@@ -142,19 +142,20 @@ void xoshiro_jump_host(uint64_t st[4], uint64_t k) {
   apply(xpow(k), st);
 }
 
-// Radix-16 jump table: out[(r * 15 + d - 1) * 4 .. +4) = x^(d * 16^r * B) mod P
-// for r < levels, d = 1..15.  A thread index t then needs one polynomial per
-// nonzero base-16 digit instead of one per set bit.
-void xoshiro_radix16_polys(uint64_t block_words, int levels, uint64_t* out) {
+// Radix-2^bits jump table: out[(r * (R - 1) + d - 1) * 4 .. +4) = x^(d * R^r * B)
+// mod P for r < levels, d = 1..R-1 (R = 2^bits).  A thread index t then needs
+// one polynomial per nonzero base-R digit instead of one per set bit.
+void xoshiro_radix_polys(uint64_t block_words, int bits, int levels, uint64_t* out) {
   std::call_once(g_once, compute_charpoly);
-  Poly q = xpow(block_words);  // x^(16^r * B) for the current level r
+  const int R = 1 << bits;
+  Poly q = xpow(block_words);  // x^(R^r * B) for the current level r
   for (int r = 0; r < levels; ++r) {
     Poly pd = q;
-    for (int d = 1; d <= 15; ++d) {
-      std::memcpy(out + ((size_t)r * 15 + d - 1) * 4, pd.w, sizeof pd.w);
+    for (int d = 1; d < R; ++d) {
+      std::memcpy(out + ((size_t)r * (R - 1) + d - 1) * 4, pd.w, sizeof pd.w);
       pd = mulmod(pd, q);
     }
-    q = pd;  // q^16
+    q = pd;  // q^R
   }
 }
 

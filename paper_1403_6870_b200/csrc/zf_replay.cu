@@ -28,6 +28,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "zf_internal.h"
@@ -437,7 +438,36 @@ __device__ __forceinline__ void xo_step(uint64_t s[4]) {
 #define ZF_XO_BLOCK 1024
 #endif
 constexpr int kXoBlock = ZF_XO_BLOCK;  // words per thread
-constexpr int kXoLevels = 10;   // radix-16 digits of the thread index (16^10 threads)
+constexpr int kXoBits = 8;      // jump-table radix 256: <= 3 polynomials for 2^24 threads
+constexpr int kXoRadix = 1 << kXoBits;
+constexpr int kXoLevels = 5;    // base-256 digits of the thread index (2^40 threads)
+
+// the jump table for B = kXoBlock, built once on the host and kept on every
+// device that used it (40 KB)
+const uint64_t* jump_table_device() {
+  static std::vector<uint64_t> host = [] {
+    std::vector<uint64_t> p((size_t)kXoLevels * (kXoRadix - 1) * 4, 0);
+    xoshiro_radix_polys(kXoBlock, kXoBits, kXoLevels, p.data());
+    return p;
+  }();
+  static std::mutex mu;
+  static std::vector<uint64_t*> per_device(64, nullptr);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!per_device[dev]) {
+    uint64_t* d = nullptr;
+    if (cudaMalloc(&d, host.size() * sizeof(uint64_t)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice) !=
+        cudaSuccess) {
+      cudaFree(d);
+      return nullptr;
+    }
+    per_device[dev] = d;
+  }
+  return per_device[dev];
+}
+
 
 // state <- (poly)(T) state: 256 generator steps, the xor of the states at the
 // poly's set coefficients (branch-free, so lanes with different polys stay
@@ -465,6 +495,16 @@ __device__ __forceinline__ void xo_apply(const unsigned long long* __restrict__ 
   s[3] = acc[3];
 }
 
+// start state of thread t's block: s0 jumped by t * kXoBlock words
+__device__ __forceinline__ void xo_jump_to(const uint64_t* __restrict__ table, uint64_t t,
+                                           uint64_t s[4]) {
+  const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(table);
+  for (int r = 0; r < kXoLevels && (t >> (kXoBits * r)) != 0; ++r) {
+    const int d = (int)((t >> (kXoBits * r)) & (kXoRadix - 1));
+    if (d) xo_apply(pp + ((size_t)r * (kXoRadix - 1) + d - 1) * 4, s);
+  }
+}
+
 // thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0, one jump
 // polynomial x^(d*16^r*B) per nonzero base-16 digit d of t; output staged
 // through a 32x32 smem tile per warp so stores are coalesced rows.
@@ -475,11 +515,7 @@ __global__ void __launch_bounds__(128)
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
-  const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(polys);
-  for (int r = 0; r < kXoLevels && (t >> (4 * r)) != 0; ++r) {
-    const int d = (int)((t >> (4 * r)) & 15);
-    if (d) xo_apply(pp + ((size_t)r * 15 + d - 1) * 4, s);
-  }
+  xo_jump_to(polys, t, s);
   const uint64_t warp_first = t - lane;  // thread index of lane 0
   for (int c = 0; c < kXoBlock; c += 32) {
 #pragma unroll 4
@@ -534,11 +570,7 @@ __global__ void __launch_bounds__(128)
   G g;
   if constexpr (GID == ZF_GEN_XOSHIRO256PP) {
     g = XoGen{{s0.x, s0.y, s0.z, s0.w}};
-    const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(polys);
-    for (int r = 0; r < kXoLevels && (t >> (4 * r)) != 0; ++r) {
-      const int d = (int)((t >> (4 * r)) & 15);
-      if (d) xo_apply(pp + ((size_t)r * 15 + d - 1) * 4, g.s);
-    }
+    xo_jump_to(polys, t, g.s);
   } else {
     g = SmGen{s0.x + t * (uint64_t)kXoBlock * kGamma};
   }
@@ -790,17 +822,11 @@ int generated_window(const zf_tables* t, int gid, const uint64_t st[4], uint64_t
   ZF_TRY(ws.alloc(&slot_cnt, T));
   ZF_TRY(ws.alloc(&overflow, 1));
   ZF_TRY(cudaMemsetAsync(overflow, 0, sizeof(unsigned int), s));
-  uint64_t* dpolys = nullptr;
+  const uint64_t* dpolys = nullptr;
   if (gid == ZF_GEN_XOSHIRO256PP) {
-    if (T - 1 >= (1ull << (4 * kXoLevels))) return ZF_ERANGE;
-    static std::vector<uint64_t> polys = [] {
-      std::vector<uint64_t> p((size_t)kXoLevels * 15 * 4, 0);
-      xoshiro_radix16_polys(kXoBlock, kXoLevels, p.data());
-      return p;
-    }();
-    ZF_TRY(ws.alloc(&dpolys, polys.size()));
-    ZF_TRY(cudaMemcpyAsync(dpolys, polys.data(), polys.size() * sizeof(uint64_t),
-                           cudaMemcpyHostToDevice, s));
+    if (T - 1 >= (1ull << (kXoBits * kXoLevels))) return ZF_ERANGE;
+    dpolys = jump_table_device();
+    if (!dpolys) return ZF_EDEVICE;
   }
   const ulonglong4 s0 = make_ulonglong4(st[0], st[1], st[2], st[3]);
   const uint64_t blocks = (T + 127) / 128;
@@ -890,26 +916,14 @@ int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cuda
   }
   if (gid != ZF_GEN_XOSHIRO256PP) return ZF_EDIST;
   const uint64_t threads = (n + kXoBlock - 1) / kXoBlock;
-  if (threads - 1 >= (1ull << (4 * kXoLevels))) return ZF_ERANGE;
-  // the radix-16 table for B = kXoBlock never changes: build it once
-  static std::vector<uint64_t> polys = [] {
-    std::vector<uint64_t> p((size_t)kXoLevels * 15 * 4, 0);
-    xoshiro_radix16_polys(kXoBlock, kXoLevels, p.data());
-    return p;
-  }();
-  uint64_t* dpolys = nullptr;
-  ZF_TRY(cudaMallocAsync(&dpolys, polys.size() * sizeof(uint64_t), s));
-  cudaError_t e = cudaMemcpyAsync(dpolys, polys.data(), polys.size() * sizeof(uint64_t),
-                                  cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) {
-    const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
-    // round the grid to whole warps so every warp's smem tile is full
-    const uint64_t blocks = (threads + 127) / 128;
-    words_xoshiro<<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
-    e = cudaGetLastError();
-  }
-  cudaFreeAsync(dpolys, s);
-  return cuda_status(e);
+  if (threads - 1 >= (1ull << (kXoBits * kXoLevels))) return ZF_ERANGE;
+  const uint64_t* dpolys = jump_table_device();
+  if (!dpolys) return ZF_EDEVICE;
+  const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
+  // round the grid to whole warps so every warp's smem tile is full
+  const uint64_t blocks = (threads + 127) / 128;
+  words_xoshiro<<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
+  return cuda_status(cudaGetLastError());
 }
 
 }  // namespace zf
