@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
 // staged; one resident wave so every warp gets ~equal numbers of chunks.
 // ---------------------------------------------------------------------------
 
-constexpr int kBatchChunk = 4;  // tiles per chunk (2048 samples at kTile 512)
+#ifndef ZF_BATCH_CHUNK
+#define ZF_BATCH_CHUNK 4
+#endif
+constexpr int kBatchChunk = ZF_BATCH_CHUNK;  // tiles per chunk (2048 samples at kTile 512)
 
 struct DevRequest {
   uint64_t seed, ctr_base, n, out_offset;
