@@ -193,8 +193,8 @@ class _SamplerBase:
         the next ``_SAMPLE_BLOCK`` values of their counter stream (one launch and
         one copy per block); the source still advances by exactly one sample per
         call, so interleaved fill() / sample() calls see the same stream as
-        repeated sample() calls.  Sequential (oracle-mode) sources draw one
-        sample per call, advancing the reference's state exactly."""
+        repeated sample() calls.  Sequential (oracle-mode) sources do the same
+        with per-draw word counts (`_sample_sequential`)."""
         src = self.source
         if src.gid != _lib.GEN_CTR:
             return self._sample_sequential(src)
@@ -226,14 +226,15 @@ class _SamplerBase:
         valid = (c is not None and c["src"] is src and c["state"] is src.state
                  and c["i"] < len(c["vals"]) and np.array_equal(c["expect"], src.state[:k]))
         if not valid:
-            probe = src.clone()
-            self.source = probe
+            self.source = src.clone()  # resolve the block on a throwaway copy
             try:
                 vals, recs = self.fill_records(self._SAMPLE_BLOCK)
             except ZigfastError:
-                return float(self._fill(1, False).item())
+                vals = None
             finally:
                 self.source = src
+            if vals is None:  # fall back to one draw on the real source
+                return float(self._fill(1, False).item())
             c = {"src": src, "state": src.state, "vals": vals.cpu().numpy(),
                  "nw": recs["nwords"].astype(np.int64), "i": 0}
             self._seq_cache = c
