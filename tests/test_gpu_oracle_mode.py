@@ -190,3 +190,21 @@ def test_scalar_samples_interleave_with_fills(zf, orc, cuda, dist):
     # an outside reseed invalidates the cached block
     s.source.state[:] = zf.UniformSource(5).state
     assert bits(np.array([s.sample()]))[0] == bits(want[:1])[0]
+
+
+def test_scalar_sample_before_a_cycling_draw(zf, golden, cuda):
+    """Replay list [255, 0, 0, w, 7] read from cursor 3: two fast draws, then
+    the wrap reaches a normal-tail draw that never finishes.  The block resolve
+    fails, sample() falls back to single draws on the real source: the first
+    two values come back with the cursor advanced, the third raises (the
+    reference would hang on it)."""
+    from paper_1403_6870_b200.errors import DeviceError
+    w = golden["kat_word"]
+    s = zf.NormalSampler(source=zf.UniformSource.replay([255, 0, 0, w, 7]), device=cuda)
+    s.source.state[0] = np.uint64(3)
+    assert_bits_equal([s.sample()], hex_to_bits(golden["kat_normal_common"]))
+    assert int(s.source.state[0]) == 4
+    s.sample()
+    assert int(s.source.state[0]) == 5
+    with pytest.raises(DeviceError):
+        s.sample()
