@@ -19,7 +19,9 @@ sm_100a library; the generator id of the source picks the kernel path:
 
 from __future__ import annotations
 
+import contextlib
 import math
+import threading
 
 import numpy as np
 
@@ -29,6 +31,51 @@ from .tables import (EXPONENTIAL, HALF_NORMAL, ZigguratTables, build_alias, defa
 from .uniform import CTR_LIMIT, UniformSource
 
 _HOST_CHUNK = 1 << 24  # samples per device chunk when the destination is host memory
+_STAGE_BYTES = 64 << 20  # bytes per pinned staging chunk (pageable host destinations)
+_STAGE_MIN_BYTES = 1 << 20  # smaller pageable fills copy directly
+
+
+class _Staging:
+    """Two pinned host buffers + two device buffers + a copy stream, kept per
+    device (pinning 128 MB costs more than the fill it serves)."""
+
+    def __init__(self, device):
+        import torch
+        self.stream = torch.cuda.Stream(device)
+        self._host = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True)
+                      for _ in range(2)]
+        self._dev = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, device=device)
+                     for _ in range(2)]
+        self.samples = 0
+
+    def host_bufs(self, dtype):
+        return [b.view(dtype) for b in self._host]
+
+    def device_bufs(self, dtype):
+        return [b.view(dtype) for b in self._dev]
+
+
+_stage_cache: dict = {}
+_stage_lock = threading.Lock()
+
+
+@contextlib.contextmanager
+def _staging(device, element_size: int):
+    """The device's cached staging set, or a private one while another thread
+    holds it."""
+    with _stage_lock:
+        entry = _stage_cache.get(device.index)
+        if entry is None:
+            entry = _stage_cache[device.index] = (_Staging(device), threading.Lock())
+    stage, lock = entry
+    if not lock.acquire(blocking=False):
+        stage, lock = _Staging(device), None
+    try:
+        stage.samples = _STAGE_BYTES // element_size
+        yield stage
+    finally:
+        if lock is not None:
+            lock.release()
 
 
 class PathCounts:
@@ -159,12 +206,20 @@ class _SamplerBase:
 
     def _fill_host(self, host, counted: bool) -> None:
         """Device fill + D2H copy, double-buffered so chunk i+1 generates while
-        chunk i copies (the copy engine is the bound for host destinations)."""
+        chunk i copies (the copy engine is the bound for host destinations).
+        Pageable destinations (a plain numpy array, the reference's usage) go
+        through pinned staging buffers instead: the driver's own pageable D2H
+        path runs at ~17 GB/s on the B200 box, a pinned copy at ~55 GB/s plus
+        a multi-threaded host memcpy at ~50 GB/s, overlapped chunk by chunk."""
         import torch
         n = host.numel()
-        chunk = min(n, _HOST_CHUNK)
         if n == 0:
             return
+        if not host.is_pinned() and n * host.element_size() >= _STAGE_MIN_BYTES:
+            with _staging(self.device, host.element_size()) as stage:
+                self._fill_staged(host, counted, stage)
+            return
+        chunk = min(n, _HOST_CHUNK)
         bufs = [torch.empty(chunk, dtype=host.dtype, device=self.device) for _ in range(2)]
         copy_stream = torch.cuda.Stream(self.device)
         compute = torch.cuda.current_stream(self.device)
@@ -184,6 +239,44 @@ class _SamplerBase:
                 ev.record(copy_stream)
                 done[b] = ev
         copy_stream.synchronize()
+
+    def _fill_staged(self, host, counted: bool, stage) -> None:
+        """Pageable host destination: generate chunk i on the device, copy it
+        D2H into pinned buffer i%2 on a side stream, and copy pinned buffer
+        (i-1)%2 into the destination on the host meanwhile."""
+        import torch
+        n = host.numel()
+        chunk = stage.samples
+        dev, pinned = stage.device_bufs(host.dtype), stage.host_bufs(host.dtype)
+        copy_stream = stage.stream
+        compute = torch.cuda.current_stream(self.device)
+        pending = []  # (event, pinned slot, destination offset, count)
+        freed = [None, None]  # device buffer b may be refilled after this event
+
+        def drain_one():
+            ev, b, off, m = pending.pop(0)
+            ev.synchronize()
+            host[off:off + m].copy_(pinned[b][:m])
+
+        for i, off in enumerate(range(0, n, chunk)):
+            m = min(chunk, n - off)
+            b = i & 1
+            if len(pending) == 2:
+                drain_one()  # pinned slot b is about to be overwritten
+            if freed[b] is not None:
+                compute.wait_event(freed[b])
+            self._launch(dev[b][:m], counted)
+            ready = torch.cuda.Event()
+            ready.record(compute)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ready)
+                pinned[b][:m].copy_(dev[b][:m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+            freed[b] = ev
+            pending.append((ev, b, off, m))
+        while pending:
+            drain_one()
 
     # -- reference API -------------------------------------------------------------
     _SAMPLE_BLOCK = 4096

@@ -109,6 +109,47 @@ def test_host_destinations(zf, orc, cuda, dist):
 
 
 @pytest.mark.parametrize("dist", DISTS)
+def test_pageable_staging_paths(zf, cuda, dist):
+    """The pinned-staging route for pageable host memory (several staging
+    chunks, ragged last one): fp32, counted fills, oracle-mode sources, CPU
+    tensors and concurrent callers all equal the device-resident fill."""
+    import threading
+    import torch
+    n32 = 3 * (16 << 20) + 5
+    a32 = np.empty(n32, dtype=np.float32)
+    sampler(zf, dist, 5, device=cuda).fill(a32)
+    d32 = torch.empty(n32, dtype=torch.float32, device=cuda)
+    sampler(zf, dist, 5, device=cuda).fill(d32)
+    assert np.array_equal(a32.view(np.uint32), d32.cpu().numpy().view(np.uint32))
+
+    n = (17 << 20) + 3
+    s_host, s_dev = sampler(zf, dist, 6, device=cuda), sampler(zf, dist, 6, device=cuda)
+    host = torch.empty(n, dtype=torch.float64)
+    s_host.fill_counted(host)
+    want = s_dev.fill_counted(n)
+    assert torch.equal(host, want.cpu())
+    assert s_host.counters.tolist() == s_dev.counters.tolist()
+
+    cls = zf.ExpSampler if dist == "exp" else zf.NormalSampler
+    o_host, o_dev = (cls(source=zf.UniformSource(8), device=cuda) for _ in range(2))
+    arr = np.empty(n)
+    o_host.fill(arr)
+    assert np.array_equal(bits(arr), bits(o_dev.fill(n).cpu().numpy()))
+    assert np.array_equal(o_host.source.state, o_dev.source.state)
+
+    outs = [np.empty(n) for _ in range(3)]
+    ths = [threading.Thread(target=lambda k=k: sampler(zf, dist, 40 + k, device=cuda).fill(outs[k]))
+           for k in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for k in range(3):
+        ref = sampler(zf, dist, 40 + k, device=cuda).fill(n).cpu().numpy()
+        assert np.array_equal(bits(outs[k]), bits(ref)), k
+
+
+@pytest.mark.parametrize("dist", DISTS)
 def test_counters_match_oracle(zf, orc, cuda, dist):
     s = sampler(zf, dist, 21, device=cuda)
     s.fill_counted(300_000)
