@@ -28,6 +28,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kPerLane = ZF_PER_LANE;  // samples per lane per tile (<= 32: mask bits)
 constexpr int kTile = 32 * kPerLane;   // samples per warp tile
 constexpr int kTileBits = kTile == 512 ? 9 : kTile == 1024 ? 10 : 8;
+constexpr int kPerLaneBits = kTileBits - 5;
 static_assert((1 << kTileBits) == kTile, "tile must be 256, 512 or 1024 samples");
 #ifndef ZF_PASS1_UNROLL
 #define ZF_PASS1_UNROLL 8
@@ -299,7 +300,6 @@ constexpr int kQueueCap = ZF_QUEUE_CAP;
 // bit-identical but slower on B200: their extra registers and code cost the
 // fast path more than they saved.)
 // A warp's whole share of a fill: tiles first_tile, first_tile + stride, ...
-// (queue entry = tile iteration << kTileBits | offset within the tile).
 template <int DIST, bool COUNTED, int P2, class Sink>
 __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
@@ -307,8 +307,13 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                                           int lane, LaneCounts& lc) {
   static_assert(P2 == 3 || P2 == 9, "unknown pass-2 policy");
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  // queue entry = tile iteration << kTileBits | lane * kPerLane | mask bit: the
+  // enqueue loop (a few lanes active) only ORs the bit in; the full-warp
+  // rounds decode the sample offset
   auto k_of = [&](uint32_t e) -> uint64_t {
-    return (first_tile + (uint64_t)(e >> kTileBits) * stride) * kTile + (e & (kTile - 1u));
+    const uint32_t off = mask_bit_offset<Sink::V>((int)(e & (kPerLane - 1u)),
+                                                  (int)((e >> kPerLaneBits) & 31u));
+    return (first_tile + (uint64_t)(e >> kTileBits) * stride) * kTile + off;
   };
   if constexpr (P2 == 9) {
     for (uint64_t tile = first_tile; tile < ntiles; tile += stride)
@@ -341,8 +346,12 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         __syncwarp();
         continue;
       }
-      for (uint32_t m = mask; m; m &= m - 1)
-        q[slot++] = (iter << kTileBits) | mask_bit_offset<Sink::V>(__ffs(m) - 1, lane);
+      const uint32_t tag = (iter << kTileBits) | ((uint32_t)lane << kPerLaneBits);
+      for (uint32_t m = mask; m;) {  // highest bit first: one FLO per entry
+        const int b = 31 - __clz(m);
+        m ^= 1u << b;
+        q[slot++] = tag | (uint32_t)b;
+      }
       qn += total;
       __syncwarp();
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 2  // cost isolation: scan + enqueue, no rounds
