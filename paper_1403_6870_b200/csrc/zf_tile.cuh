@@ -279,6 +279,17 @@ __device__ __forceinline__ int warp_excl_count(int mine, int lane, int* total) {
   return __popc(b0 & lt) + 2 * __popc(b1 & lt);
 }
 
+// The same from the lane masks themselves: when no lane holds two or more
+// exceptional samples (~60 % of 512-sample tiles) one ballot of "any" decides
+// the prefix; otherwise the bit-plane count above.
+__device__ __forceinline__ int warp_excl_mask(uint32_t mask, int lane, int* total) {
+  const uint32_t multi = __ballot_sync(0xffffffffu, (mask & (mask - 1u)) != 0u);
+  if (multi) return warp_excl_count(__popc(mask), lane, total);
+  const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
+  *total = __popc(any);
+  return __popc(any & ((1u << lane) - 1u));
+}
+
 template <int V>
 __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
   return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
@@ -329,7 +340,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
 #ifdef ZF_SHFL_SCAN
       int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
 #else
-      int slot = qn + warp_excl_count(__popc(mask), lane, &total);
+      int slot = qn + warp_excl_mask(mask, lane, &total);
 #endif
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 1  // cost isolation: scan only
       if (total == 12345) q[lane] = slot;
