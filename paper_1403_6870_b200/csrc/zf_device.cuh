@@ -28,9 +28,31 @@ constexpr uint64_t kExcBase = 1ull << 63;
 constexpr int kExcShift = 19;
 constexpr int kSlots = 256;
 
+// z * c mod 2^64 in three IMADs: nvcc's own expansion adds the two cross
+// products separately and then folds them into the high word (four IMADs);
+// the fill kernel is issue-bound, so the chained form saves one instruction
+// per multiply (two per word).
+template <uint64_t C>
+__device__ __forceinline__ uint64_t mul64_chained(uint64_t z) {
+  const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  uint32_t rlo, rhi;
+  asm("mul.lo.u32 %0, %2, %4;\n\t"
+      "mul.hi.u32 %1, %2, %4;\n\t"
+      "mad.lo.u32 %1, %2, %5, %1;\n\t"
+      "mad.lo.u32 %1, %3, %4, %1;"
+      : "=&r"(rlo), "=&r"(rhi)
+      : "r"(lo), "r"(hi), "n"((uint32_t)C), "n"((uint32_t)(C >> 32)));
+  return ((uint64_t)rhi << 32) | rlo;
+}
+
 __host__ __device__ __forceinline__ uint64_t mix13(uint64_t z) {
+#if defined(__CUDA_ARCH__) && !defined(ZF_PLAIN_MUL64)
+  z = mul64_chained<kM1>(z ^ (z >> 30));
+  z = mul64_chained<kM2>(z ^ (z >> 27));
+#else
   z = (z ^ (z >> 30)) * kM1;
   z = (z ^ (z >> 27)) * kM2;
+#endif
   return z ^ (z >> 31);
 }
 
