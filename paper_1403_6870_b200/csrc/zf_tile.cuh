@@ -282,8 +282,10 @@ __device__ __forceinline__ int warp_excl_count(int mine, int lane, int* total) {
 // The same from the lane masks themselves: when no lane holds two or more
 // exceptional samples (~60 % of 512-sample tiles) one ballot of "any" decides
 // the prefix; otherwise the bit-plane count above.
-__device__ __forceinline__ int warp_excl_mask(uint32_t mask, int lane, int* total) {
+__device__ __forceinline__ int warp_excl_mask(uint32_t mask, int lane, int* total,
+                                              bool* multi_any = nullptr) {
   const uint32_t multi = __ballot_sync(0xffffffffu, (mask & (mask - 1u)) != 0u);
+  if (multi_any) *multi_any = multi != 0u;
   if (multi) return warp_excl_count(__popc(mask), lane, total);
   const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
   *total = __popc(any);
@@ -333,15 +335,13 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
   } else {
     int qn = 0;  // warp-uniform queue length
     uint32_t iter = 0;
+    const uint32_t qs = (uint32_t)__cvta_generic_to_shared(q);
     for (uint64_t tile = first_tile; tile < ntiles; tile += stride, ++iter) {
       const uint32_t mask =
           fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
       int total;
-#ifdef ZF_SHFL_SCAN
-      int slot = qn + warp_excl_scan(__popc(mask), lane, &total);
-#else
-      int slot = qn + warp_excl_mask(mask, lane, &total);
-#endif
+      bool multi;  // some lane holds two or more exceptions
+      int slot = qn + warp_excl_mask(mask, lane, &total, &multi);
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 1  // cost isolation: scan only
       if (total == 12345) q[lane] = slot;
       continue;
@@ -358,10 +358,23 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         continue;
       }
       const uint32_t tag = (iter << kTileBits) | ((uint32_t)lane << kPerLaneBits);
-      for (uint32_t m = mask; m;) {  // highest bit first: one FLO per entry
-        const int b = 31 - __clz(m);
-        m ^= 1u << b;
-        q[slot++] = tag | (uint32_t)b;
+      {
+        // every lane's highest entry with one predicated shared store (no
+        // divergent block); the loop runs only when some lane holds two or
+        // more (~40 % of tiles) and then only for the rest of the bits
+        const int hb = 31 - __clz(mask);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                     "@p st.shared.u32 [%0], %1;\n\t}"
+                     ::"r"(qs + 4u * (uint32_t)slot), "r"(tag | (uint32_t)hb), "r"(mask)
+                     : "memory");
+        if (multi) {
+          ++slot;
+          for (uint32_t m = mask & ~(0x80000000u >> __clz(mask)); m;) {
+            const int b = 31 - __clz(m);
+            m ^= 1u << b;
+            q[slot++] = tag | (uint32_t)b;
+          }
+        }
       }
       qn += total;
       __syncwarp();
