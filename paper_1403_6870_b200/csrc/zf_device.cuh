@@ -331,6 +331,32 @@ __device__ double exp_draw(const DevPack& p, uint64_t u, S& s, C& c, double shif
   }
 }
 
+// One attempt of the normal overhang box loop (_kernels.py:679-688) for slot j
+// from the stream's current position: true and x if accepted.
+template <class S>
+__device__ __forceinline__ bool normal_box_attempt(const DevPack& h, int j, S& s, double& x) {
+  const double ux = u01(s.next());
+  const double uy = u01(s.next());
+  x = __dadd_rn(h.xlo[j], __dmul_rn(ux, h.xw[j]));
+  const double y = __dadd_rn(h.flo[j], __dmul_rn(uy, h.fh[j]));
+  return less_than_exp(y, __dmul_rn(__dmul_rn(-0.5, x), x));
+}
+
+// Normal tail beyond r = X[1] (_kernels.py:611-678): Marsaglia's method with
+// two embedded exponential-ziggurat draws per attempt (not counted, :516-517).
+template <class S, class C>
+__device__ __forceinline__ double normal_tail(const DevPack& h, const DevPack& e, S& s, C& c) {
+  NoCount quiet;
+  for (;;) {
+    if (C::kOn) c.attempts++;
+    const double e1 = exp_draw(e, s.next(), s, quiet);
+    const double e2 = exp_draw(e, s.next(), s, quiet);
+    if (S::kBounded && s.dead()) return 0.0;
+    const double x = __ddiv_rn(e1, h.tailx);
+    if (__dadd_rn(e2, e2) > __dmul_rn(x, x)) return __dadd_rn(h.tailx, x);
+  }
+}
+
 // Normal draw from its first word `u` (normal_one_counted, _kernels.py:498-594).
 // The embedded exponential draws of the tail are not counted (:516-517).
 template <class S, class C>
@@ -348,18 +374,8 @@ __device__ double normal_draw(const DevPack& h, const DevPack& e, uint64_t u, S&
   if (j == 0) {
     c.add(4);
     c.path |= ZF_PATH_TAIL;
-    NoCount quiet;
-    for (;;) {
-      if (C::kOn) c.attempts++;
-      const double e1 = exp_draw(e, s.next(), s, quiet);
-      const double e2 = exp_draw(e, s.next(), s, quiet);
-      if (S::kBounded && s.dead()) return 0.0;
-      const double x = __ddiv_rn(e1, h.tailx);
-      if (__dadd_rn(e2, e2) > __dmul_rn(x, x)) {
-        val = __dadd_rn(h.tailx, x);
-        break;
-      }
-    }
+    val = normal_tail(h, e, s, c);
+    if (S::kBounded && s.dead()) return 0.0;
   } else {
     for (;;) {
       c.add(5);

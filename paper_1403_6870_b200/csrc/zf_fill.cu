@@ -25,6 +25,9 @@
 
 namespace zf {
 
+// the per-warp queues (and their 16-byte round scratch) follow the staged packs
+static_assert(sizeof(DevPack) % 16 == 0 && sizeof(DevTables) % 16 == 0, "queue alignment");
+
 // Default pass-2 policy (measured): recursive rounds of 32 have
 // the smallest code and register footprint and win for both distributions.
 template <int DIST, bool COUNTED>
@@ -46,7 +49,7 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
   stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   const int lane = threadIdx.x & 31;
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kPacks * sizeof(DevPack)) +
-                    (threadIdx.x >> 5) * kQueueCap;
+                    (threadIdx.x >> 5) * kQueueWords;
   __syncthreads();
   const DevPack& P = sp[0];
   const DevPack& E = sp[kPacks - 1];
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kThreads)
   stage_block(st, gt, (int)sizeof(DevTables));
   const int lane = threadIdx.x & 31;
   uint32_t* queue =
-      reinterpret_cast<uint32_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kQueueCap;
+      reinterpret_cast<uint32_t*>(smem_raw + sizeof(DevTables)) + (threadIdx.x >> 5) * kQueueWords;
   __syncthreads();
   LaneCounts lc;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
@@ -155,7 +158,7 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
     if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
     if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
   }
-  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
+  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
@@ -203,7 +206,7 @@ static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq,
                               const uint32_t* chunk_req, uint64_t total_chunks, OutT* out,
                               cudaStream_t s) {
   auto kernel = fill_batch_kernel<OutT, VEC>;
-  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kQueueCap * sizeof(uint32_t);
+  const size_t smem = sizeof(DevTables) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
   int grid = 0;
   // one resident wave: every warp loops over ~equal numbers of whole chunks
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_chunks, &grid, 1));

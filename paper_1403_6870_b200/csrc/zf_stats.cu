@@ -29,6 +29,8 @@ struct StatsShared {
   double thresh[8];
   double warp_sums[kWarps][5];
 };
+// the per-warp queues (and their 16-byte round scratch) follow it
+static_assert(sizeof(StatsShared) % 16 == 0, "queue alignment");
 
 template <bool EXTRA>
 __device__ void init_sink(StatsSinkT<EXTRA>& k, StatsShared* sh, unsigned int* hist,
@@ -108,8 +110,8 @@ __global__ void __launch_bounds__(kThreads)
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
   StatsShared* sh = reinterpret_cast<StatsShared*>(smem_raw + kPacks * sizeof(DevPack));
   uint32_t* queues = reinterpret_cast<uint32_t*>(sh + 1);
-  uint32_t* queue = queues + (threadIdx.x >> 5) * kQueueCap;
-  unsigned int* hist = queues + kWarps * kQueueCap;
+  uint32_t* queue = queues + (threadIdx.x >> 5) * kQueueWords;
+  unsigned int* hist = queues + kWarps * kQueueWords;
   stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -189,7 +191,7 @@ int launch_fill_stats_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base,
   const uint32_t grid = stats_blocks(n);
   const int mode = sum_only(cfg) ? 0 : extra(cfg) ? 2 : 1;
   const size_t smem = kPacks * sizeof(DevPack) + sizeof(StatsShared) +
-                      (size_t)kWarps * kQueueCap * sizeof(uint32_t) + hist_bytes(cfg);
+                      (size_t)kWarps * kQueueWords * sizeof(uint32_t) + hist_bytes(cfg);
   auto kern = mode == 0   ? fill_stats_kernel<DIST, 0>
               : mode == 1 ? fill_stats_kernel<DIST, 1>
                           : fill_stats_kernel<DIST, 2>;

@@ -35,6 +35,18 @@ static_assert((1 << kTileBits) == kTile, "tile must be 256, 512 or 1024 samples"
 #endif
 constexpr int kPass1Unroll = ZF_PASS1_UNROLL;
 
+#ifndef ZF_QUEUE_CAP
+#define ZF_QUEUE_CAP 128
+#endif
+constexpr int kQueueCap = ZF_QUEUE_CAP;
+// Normal rounds of 32 use warp-cooperative box attempts (resolve_round_normal);
+// ZF_COOP=0 builds the plain recursive rounds for A/B runs.
+#ifndef ZF_COOP
+#define ZF_COOP 1
+#endif
+// per-warp shared words: the queue, then 32 x 16 B of round scratch
+constexpr int kQueueWords = kQueueCap + (ZF_COOP ? 128 : 0);
+
 template <typename OutT>
 struct VecOf;
 template <>
@@ -253,6 +265,83 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
   sink.put(k, to_out<OutT>(v), false);
 }
 
+// kSlotLanes[r]: bits 0, r, 2r, ... below 32 (the lanes serving slot 0 of r)
+__constant__ const uint32_t kSlotLanes[33] = {
+    0u,          0xFFFFFFFFu, 0x55555555u, 0x49249249u, 0x11111111u, 0x42108421u, 0x41041041u,
+    0x10204081u, 0x01010101u, 0x08040201u, 0x40100401u, 0x00400801u, 0x01001001u, 0x04002001u,
+    0x10004001u, 0x40008001u, 0x00010001u, 0x00020001u, 0x00040001u, 0x00080001u, 0x00100001u,
+    0x00200001u, 0x00400001u, 0x00800001u, 0x01000001u, 0x02000001u, 0x04000001u, 0x08000001u,
+    0x10000001u, 0x20000001u, 0x40000001u, 0x80000001u, 0x00000001u};
+// A full round of 32 normal draws (one queued sample k per lane) with
+// warp-cooperative box attempts.  Every lane first makes its own sample's
+// alias pick and first box attempt, as the sequential loop does.  Then, while
+// r samples are unresolved, lane L works on unresolved sample L mod r and
+// evaluates its attempt number next + L / r: the words of attempt a of sample
+// K sit at fixed positions 3 + 2a, 4 + 2a of K's secondary counter stream, so
+// any lane can evaluate any attempt.  A sample takes its accepted attempt with
+// the lowest index (the lowest accepting lane of its slot) -- exactly the one
+// the sequential loop would stop at -- and otherwise advances `next` by the
+// number of lanes that served it.  Owners publish (stream base, j, next) in
+// `own` (32 x 16 B of per-warp shared scratch); a round takes ~2-3 iterations
+// where the one-sample-per-lane loop waits ~5.4 for its slowest lane.
+template <class Sink>
+__device__ __forceinline__ void resolve_round_normal(const DevPack& P, const DevPack& E,
+                                                     uint64_t seed, uint64_t ctr_base, Sink& sink,
+                                                     uint64_t k, int lane, uint32_t* own) {
+  // (own must be 16-byte aligned: kQueueCap words past a 16-byte aligned queue)
+  using OutT = typename Sink::Out;
+  const uint64_t K = ctr_base + k;
+  const uint64_t u = mix13(seed + (K + 1) * kGamma);  // the sign word
+  const uint64_t sbase = seed + (kExcBase + (K << kExcShift)) * kGamma;
+  CtrStream s{sbase};
+  const int j = alias_pick(P, s);
+  double val;
+  bool done;
+  if (j == 0) {
+    NoCount c;
+    val = normal_tail(P, E, s, c);
+    done = true;
+  } else {
+    done = normal_box_attempt(P, j, s, val);
+  }
+  uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t un = __ballot_sync(0xffffffffu, !done); un;
+       un = __ballot_sync(0xffffffffu, !done)) {
+    const int r = __popc(un);
+    const int rank = __popc(un & lt);  // my slot if unresolved
+    // owners publish (stream base, slot j, next attempt) at their rank
+    if (!done)
+      reinterpret_cast<uint4*>(own)[rank] =
+          make_uint4((uint32_t)sbase, (uint32_t)(sbase >> 32), (uint32_t)j, next);
+    __syncwarp();
+    // lane / r and lane % r without an integer division: (lane + 0.5) / r is
+    // at least 1/64 away from an integer, far above the reciprocal's error
+    const int qd = __float2int_rz(__fmul_rn((float)lane + 0.5f, __frcp_rn((float)r)));
+    const uint4 st4 = reinterpret_cast<const uint4*>(own)[lane - qd * r];
+    __syncwarp();
+    const uint64_t sb = ((uint64_t)st4.y << 32) | st4.x;
+    const int jo = (int)st4.z;
+    const uint32_t a = st4.w + (uint32_t)qd;
+    CtrStream t{sb + (uint64_t)(2 + 2 * a) * kGamma};
+    double x;
+    const bool acc = normal_box_attempt(P, jo, t, x);
+    const uint32_t A = __ballot_sync(0xffffffffu, acc);
+    // lanes serving slot `rank`: rank, rank + r, rank + 2r, ...
+    const uint32_t mine = kSlotLanes[r] << rank;
+    const uint32_t hits = done ? 0u : (A & mine);
+    const int w = hits ? __ffs(hits) - 1 : lane;
+    const double xw = __shfl_sync(0xffffffffu, x, w);
+    if (hits) {
+      val = xw;
+      done = true;
+    } else if (!done) {
+      next += (uint32_t)__popc(mine);
+    }
+  }
+  sink.put(k, to_out<OutT>((long long)u < 0 ? -val : val), false);
+}
+
 // Exclusive warp prefix of `mine`; returns it and sets *total (warp-uniform).
 __device__ __forceinline__ int warp_excl_scan(int mine, int lane, int* total) {
   int incl = mine;
@@ -300,10 +389,6 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
 // Per-warp queue words: < 32 leftovers + the exceptions of one tile (~15 on
 // average for 1024 samples); a tile that would overflow is resolved in place.
 // Small on purpose: shared memory, not registers, limits CTAs per SM.
-#ifndef ZF_QUEUE_CAP
-#define ZF_QUEUE_CAP 128
-#endif
-constexpr int kQueueCap = ZF_QUEUE_CAP;
 
 // Pass-2 policies (template parameter P2 of run_tiles), all bit-identical:
 //   3  rounds of exactly 32 recursive draws as soon as 32 are queued
@@ -385,7 +470,15 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       if (qn < 32) continue;
       int done = 0;
       for (; qn - done >= 32; done += 32)
-        resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
+      {
+        if constexpr (ZF_COOP && DIST == ZF_NORMAL && !COUNTED) {
+          const uint32_t tag = q[done + lane];
+          __syncwarp();
+          resolve_round_normal(P, E, seed, ctr_base, sink, k_of(tag), lane, q + kQueueCap);
+        } else {
+          resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[done + lane]), lc);
+        }
+      }
       __syncwarp();
       for (int j = lane; j < qn - done; j += 32) q[j] = q[j + done];
       qn -= done;
