@@ -81,8 +81,12 @@ struct DevRequest {
   int32_t dist, pad;
 };
 
+#ifndef ZF_BATCH_MIN_BLOCKS
+#define ZF_BATCH_MIN_BLOCKS 1
+#endif
+
 template <typename OutT, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, ZF_BATCH_MIN_BLOCKS)
     fill_batch_kernel(const DevTables* __restrict__ gt, const DevRequest* __restrict__ reqs,
                       const uint32_t* __restrict__ chunk_req, uint64_t total_chunks,
                       OutT* __restrict__ out) {
@@ -223,26 +227,34 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
   // every request must keep 16-byte alignment for the vector path
   bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   std::vector<DevRequest> h((size_t)nreq);
-  uint64_t chunks = 0;
+  // chunk ids: every exponential request's chunks first, then the normal ones.
+  // A warp strides through the ids, so it switches distribution at most once
+  // instead of at every chunk (requests usually alternate): with alternating
+  // chunks a third of the stalls were instruction fetches
+  uint64_t per_dist[2] = {0, 0};
   for (int i = 0; i < nreq; ++i) {
     const zf_request& r = reqs[i];
     if (r.dist != ZF_EXP && r.dist != ZF_NORMAL) return ZF_EDIST;
     if (r.ctr_base > kMaxCtr || r.n > kMaxCtr - r.ctr_base) return ZF_ERANGE;
     if ((r.out_offset * esz) & 15) vec = false;
-    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, chunks, r.dist, 0};
-    chunks += ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;  // chunks
+    per_dist[r.dist] += ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;
   }
+  const uint64_t chunks = per_dist[0] + per_dist[1];
   if (chunks == 0) return ZF_OK;
   if (chunks > 0xFFFFFFFFull) return ZF_ERANGE;
   // one upload: the request table, then the chunk -> request map
   const size_t req_bytes = sizeof(DevRequest) * (size_t)nreq;
   std::vector<unsigned char> blob(req_bytes + sizeof(uint32_t) * chunks);
-  std::memcpy(blob.data(), h.data(), req_bytes);
   uint32_t* cmap = reinterpret_cast<uint32_t*>(blob.data() + req_bytes);
+  uint64_t next[2] = {0, per_dist[0]};
   for (int i = 0; i < nreq; ++i) {
-    const uint64_t end = i + 1 < nreq ? h[i + 1].chunk_begin : chunks;
-    for (uint64_t c = h[i].chunk_begin; c < end; ++c) cmap[c] = (uint32_t)i;
+    const zf_request& r = reqs[i];
+    const uint64_t nc = ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;
+    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, next[r.dist], r.dist, 0};
+    for (uint64_t c = 0; c < nc; ++c) cmap[next[r.dist] + c] = (uint32_t)i;
+    next[r.dist] += nc;
   }
+  std::memcpy(blob.data(), h.data(), req_bytes);
   unsigned char* d = nullptr;
   ZF_TRY(cudaMallocAsync(&d, blob.size(), s));
   // pageable source: the runtime stages it before returning, so `blob` may die
