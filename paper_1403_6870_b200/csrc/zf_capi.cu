@@ -193,6 +193,11 @@ int zf_trad_tables_create_default(int device, zf_tables** out) {
 int zf_tables_destroy(zf_tables* t) {
   if (!t) return ZF_OK;
   cudaError_t e = cudaFree(t->dev);
+  for (auto& sl : t->stage.slot) {
+    if (sl.done) cudaEventSynchronize(sl.done), cudaEventDestroy(sl.done);
+    if (sl.host) cudaFreeHost(sl.host);
+    if (sl.dev) cudaFree(sl.dev);
+  }
   delete t;
   return cuda_status(e);
 }

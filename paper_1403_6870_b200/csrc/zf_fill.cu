@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "zf_internal.h"
@@ -242,10 +243,35 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
   const uint64_t chunks = per_dist[0] + per_dist[1];
   if (chunks == 0) return ZF_OK;
   if (chunks > 0xFFFFFFFFull) return ZF_ERANGE;
-  // one upload: the request table, then the chunk -> request map
+  // one upload: the request table, then the chunk -> request map, staged in
+  // the handle's pinned ring slot
   const size_t req_bytes = sizeof(DevRequest) * (size_t)nreq;
-  std::vector<unsigned char> blob(req_bytes + sizeof(uint32_t) * chunks);
-  uint32_t* cmap = reinterpret_cast<uint32_t*>(blob.data() + req_bytes);
+  const size_t bytes = req_bytes + sizeof(uint32_t) * chunks;
+  std::lock_guard<std::mutex> lock(t->stage.mu);
+  BatchStage& sl = t->stage.slot[t->stage.next];
+  t->stage.next = (t->stage.next + 1) % kStageSlots;
+  if (sl.done) ZF_TRY(cudaEventSynchronize(sl.done));  // its previous batch has read it
+  if (sl.cap < bytes || !sl.done) {  // (re)allocate on the handle's device
+    int prev = 0;
+    ZF_TRY(cudaGetDevice(&prev));
+    ZF_TRY(cudaSetDevice(t->device));
+    cudaError_t e = cudaSuccess;
+    if (sl.cap < bytes) {
+      const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+      if (sl.host) cudaFreeHost(sl.host);
+      if (sl.dev) cudaFree(sl.dev);
+      sl.host = nullptr;
+      sl.dev = nullptr;
+      sl.cap = 0;
+      e = cudaMallocHost(&sl.host, cap);
+      if (e == cudaSuccess) e = cudaMalloc(&sl.dev, cap);
+      if (e == cudaSuccess) sl.cap = cap;
+    }
+    if (e == cudaSuccess && !sl.done) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
+    cudaSetDevice(prev);
+    ZF_TRY(e);
+  }
+  uint32_t* cmap = reinterpret_cast<uint32_t*>(sl.host + req_bytes);
   uint64_t next[2] = {0, per_dist[0]};
   for (int i = 0; i < nreq; ++i) {
     const zf_request& r = reqs[i];
@@ -254,23 +280,19 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
     for (uint64_t c = 0; c < nc; ++c) cmap[next[r.dist] + c] = (uint32_t)i;
     next[r.dist] += nc;
   }
-  std::memcpy(blob.data(), h.data(), req_bytes);
-  unsigned char* d = nullptr;
-  ZF_TRY(cudaMallocAsync(&d, blob.size(), s));
-  // pageable source: the runtime stages it before returning, so `blob` may die
-  cudaError_t e = cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, s);
-  int status = (int)e;
-  if (e == cudaSuccess) {
-    const DevRequest* dr = reinterpret_cast<const DevRequest*>(d);
-    const uint32_t* dm = reinterpret_cast<const uint32_t*>(d + req_bytes);
-    if (dtype == ZF_F64)
-      status = vec ? launch_batch_typed<double, true>(t, dr, dm, chunks, (double*)out, s)
-                   : launch_batch_typed<double, false>(t, dr, dm, chunks, (double*)out, s);
-    else
-      status = vec ? launch_batch_typed<float, true>(t, dr, dm, chunks, (float*)out, s)
-                   : launch_batch_typed<float, false>(t, dr, dm, chunks, (float*)out, s);
-  }
-  cudaFreeAsync(d, s);
+  std::memcpy(sl.host, h.data(), req_bytes);
+  ZF_TRY(cudaMemcpyAsync(sl.dev, sl.host, bytes, cudaMemcpyHostToDevice, s));
+  const DevRequest* dr = reinterpret_cast<const DevRequest*>(sl.dev);
+  const uint32_t* dm = reinterpret_cast<const uint32_t*>(sl.dev + req_bytes);
+  int status;
+  if (dtype == ZF_F64)
+    status = vec ? launch_batch_typed<double, true>(t, dr, dm, chunks, (double*)out, s)
+                 : launch_batch_typed<double, false>(t, dr, dm, chunks, (double*)out, s);
+  else
+    status = vec ? launch_batch_typed<float, true>(t, dr, dm, chunks, (float*)out, s)
+                 : launch_batch_typed<float, false>(t, dr, dm, chunks, (float*)out, s);
+  const cudaError_t er = cudaEventRecord(sl.done, s);
+  if (status == ZF_OK && er != cudaSuccess) status = (int)er;
   return status;
 }
 

@@ -3,8 +3,28 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "zf_device.cuh"
+
+namespace zf {
+// Request-table staging for zf_fill_batch: a ring of pinned host + device
+// buffer pairs reused across calls (no cudaMallocAsync and no pageable copy
+// per call).  A slot is refilled only after the event recorded behind the
+// launches that read it has completed.
+struct BatchStage {
+  unsigned char* host = nullptr;  // pinned
+  unsigned char* dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+constexpr int kStageSlots = 2;
+struct StageRing {
+  std::mutex mu;
+  BatchStage slot[kStageSlots];
+  int next = 0;
+};
+}  // namespace zf
 
 struct zf_tables {
   int kind;  // zf::kKindModified or zf::kKindTraditional
@@ -12,6 +32,7 @@ struct zf_tables {
   int sm_count;
   zf::DevTables* dev;  // device copy: half-normal pack then exponential pack
   zf::DevTables host;  // host mirror (used by tests of the pack layout)
+  mutable zf::StageRing stage;
 };
 
 namespace zf {

@@ -176,6 +176,25 @@ def test_batch_matches_individual_fills(zf, orc, cuda):
         assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
 
 
+def test_batch_staging_ring_reuse(zf, orc, cuda):
+    """Back-to-back batches on one tables handle without host syncs: the
+    request tables go through the handle's reused pinned/device staging slots
+    (which grow with the batch), so every batch must still see its own table."""
+    import torch
+    plans, outs = [], []
+    for b, m in enumerate((3, 40, 7, 300, 300, 12)):  # grows, shrinks, grows past capacity
+        reqs = [("normal" if (i + b) % 3 else "exp", 700 + 97 * i, 1000 * b + i) for i in range(m)]
+        plan = zf.BatchPlan([r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs])
+        plans.append((plan, reqs))
+        outs.append(plan.fill(device=cuda))  # no synchronize between batches
+    torch.cuda.synchronize(cuda)
+    for (plan, reqs), out in zip(plans, outs):
+        host = out.cpu().numpy()
+        for (dist, n, seed), off in zip(reqs[::17], plan.offsets[::17]):
+            want, _, _ = orc.fill_ctr(dist, n, seed=seed)
+            assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
+
+
 def test_convenience_api(zf, cuda):
     zf.seed(2024)
     a = zf.normal(1000, device=cuda)
