@@ -208,8 +208,6 @@ int zf_xoshiro_jump(uint64_t* state, uint64_t k);
  * xoshiro256 state transition (e = 128 gives the published jump() constants). */
 int zf_xoshiro_pow2_poly(int e, uint64_t* out4);
 
-/* Batched production fill: one launch for all requests (requests in host
- * memory, copied by the call).  dtype applies to all requests. */
 /* Text output of the reference's `gen --format text` (cli.py:100-120):
  * writes "".join(f"{v:.17g}\n" for v in x) -- byte-identical to CPython's
  * '%.17g' -- for n doubles at x_dev into out_dev (capacity `cap` bytes;
@@ -222,6 +220,14 @@ int zf_format_g17(const double* x_dev, uint64_t n, char* out_dev, uint64_t cap,
                   uint64_t* scratch_dev, void* stream);
 uint64_t zf_format_scratch_words(uint64_t n);
 
+/* Batched production fill (many `Sampler(...).fill(n)` requests,
+ * exponential.py:45-50): one launch for all requests; request r fills
+ * out_dev[out_offset_r ...] with samples ctr_base_r .. ctr_base_r + n_r - 1 of
+ * its seed's counter stream.  dtype applies to all requests.  The request
+ * table is copied by the call into the handle's pinned staging ring (two
+ * slots, reused behind CUDA events), so `reqs` may be freed on return; the
+ * call blocks only when the slot it needs still feeds the batch two calls
+ * back.  Thread-safe per handle.  Asynchronous otherwise. */
 int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                   void* out_dev, void* stream);
 

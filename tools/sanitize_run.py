@@ -20,5 +20,8 @@ for cls in (zf.ExpSampler, zf.NormalSampler):
     r = cls(source=zf.UniformSource.replay([255, 0, 0, 123456789 << 8]), device=dev)
     r.fill(100)
 zf.fill_batch([("exp", 1000, 1), ("normal", 8192, 2), ("exp", 3, 3)], device=dev)
+# staging-ring reuse and growth, cooperative normal rounds in the batch kernel
+zf.fill_batch([("normal", 20_000 + i, 10 + i) for i in range(40)], device=dev)
+zf.fill_batch([("exp", 5, 1)], device=dev)
 torch.cuda.synchronize()
 print("sanitize run ok")
