@@ -132,14 +132,22 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
   if (e != cudaSuccess) return (int)e;
   per_sm = std::max(per_sm, 1);
   const uint64_t want = (ntiles + kWarps - 1) / kWarps;
-  // ZF_GRID_WAVES=w (default 4): w waves of resident CTAs; shorter per-warp
-  // tile runs balance the tail of the launch better than one persistent wave
-  static const int waves = [] {
+  // ZF_GRID_WAVES=w overrides the number of resident waves per launch; by
+  // default it grows with the fill (measured on B200, normal / exp G/s at the
+  // chosen value vs 4 waves: 2^26 samples 4 waves; 2^28 6 waves, 633 / 663 vs
+  // 624 / 659; 2^30 8 waves, 629 / 637 vs 605 / 630; 2^32 12 waves, 631 / 656
+  // vs 602 / 622 -- tools/ab_waves_n.sh)
+  static const int env_waves = [] {
     const char* e = getenv("ZF_GRID_WAVES");
-    return e ? std::max(1, atoi(e)) : 4;
+    return e ? std::max(1, atoi(e)) : 0;
   }();
-  *grid = (int)std::min<uint64_t>(want,
-                                  (uint64_t)per_sm * sm_count * (fixed_waves ? fixed_waves : waves));
+  const int waves = fixed_waves ? fixed_waves
+                    : env_waves ? env_waves
+                    : ntiles <= (1ull << 17) ? 4
+                    : ntiles <= (1ull << 19) ? 6
+                    : ntiles <= (1ull << 21) ? 8
+                                             : 12;
+  *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count * waves);
   if (*grid < 1) *grid = 1;
   return ZF_OK;
 }
