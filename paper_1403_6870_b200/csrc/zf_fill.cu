@@ -82,6 +82,9 @@ struct DevRequest {
   int32_t dist, pad;
 };
 
+#ifndef ZF_BATCH_WAVES
+#define ZF_BATCH_WAVES 1  // resident waves of the batch kernel
+#endif
 #ifndef ZF_BATCH_MIN_BLOCKS
 #define ZF_BATCH_MIN_BLOCKS 1
 #endif
@@ -222,7 +225,7 @@ static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq,
   const size_t smem = sizeof(DevTables) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
   int grid = 0;
   // one resident wave: every warp loops over ~equal numbers of whole chunks
-  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_chunks, &grid, 1));
+  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, total_chunks, &grid, ZF_BATCH_WAVES));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, dreq, chunk_req, total_chunks, out);
   return cuda_status(cudaGetLastError());
 }
