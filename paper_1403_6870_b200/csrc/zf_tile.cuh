@@ -453,11 +453,32 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                      ::"r"(qs + 4u * (uint32_t)slot), "r"(tag | (uint32_t)hb), "r"(mask)
                      : "memory");
         if (multi) {
+          if constexpr (DIST == ZF_EXP) {
+          // exponential (1.56 % exceptional: a lane holds two in ~57 % of
+          // tiles): the second entry is predicated as well and the loop runs
+          // only for lanes with three or more.  (The normal kernel loses 6 %
+          // with it: +4 registers and a worse layout.)
+          const uint32_t m2 = mask & ~(0x80000000u >> __clz(mask));
+          const int hb2 = 31 - __clz(m2);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                       "@p st.shared.u32 [%0], %1;\n\t}"
+                       ::"r"(qs + 4u * (uint32_t)(slot + 1)), "r"(tag | (uint32_t)hb2), "r"(m2)
+                       : "memory");
+          if (__ballot_sync(0xffffffffu, (m2 & (m2 - 1u)) != 0u)) {
+            slot += 2;
+            for (uint32_t m = m2 & ~(0x80000000u >> __clz(m2)); m;) {
+              const int b = 31 - __clz(m);
+              m ^= 1u << b;
+              q[slot++] = tag | (uint32_t)b;
+            }
+          }
+          } else {
           ++slot;
           for (uint32_t m = mask & ~(0x80000000u >> __clz(mask)); m;) {
             const int b = 31 - __clz(m);
             m ^= 1u << b;
             q[slot++] = tag | (uint32_t)b;
+          }
           }
         }
       }
