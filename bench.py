@@ -3,23 +3,31 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Workload (BASELINE.json config 2): N(0,1) fp64, n = 2^28 samples per GPU per
-step, seed 1234, production counter stream; GPU g starts at counter g*2^40
-(config 3's sharding rule, weak scaling, no collective on the hot path).  One
-step = one `NormalSampler.fill(out)` = one kernel launch writing 2 GiB (larger
-than the 126 MB L2, so no flush is needed between steps).  The exponential
-sampler is timed the same way and reported beside it.
+Workload (BASELINE.json config 3, the configuration the metric is quoted on):
+N(0,1) fp64, n = 2^32 samples per GPU per step, seed 7, production counter
+stream, GPU g at counter g*2^40 (weak scaling, no collective on the hot path;
+the only collective is a SUM allreduce of the validation statistics).  One
+step = one `NormalSampler.fill(out)` = one kernel launch writing 32 GiB (far
+larger than the 126 MB L2, so no flush is needed between steps).  The
+headline leg runs first, on a GPU that has been idle, before the other legs:
+exponential fills and generate-and-sum at the same n, the config-2
+validation (2^28, seed 1234), the config-5 tail-stress leg (2^36 draws per
+distribution over all ranks, generate-and-count), e2e legs and the CPU
+baseline.
 
 Roofline: algorithmic bytes = 8 B per fp64 sample written, 0 B read; achieved
 GB/s = 8 n / (CUDA-event kernel time) against MEASURED_PEAKS.json hbm_gbs (a
 copy), and against a write-only peak measured live on the same GPU.
 
-e2e: the same metric through the public API into a pinned host buffer
-(generation + D2H copy inside the timed region, double-buffered).
+e2e: the same metric through the public API into HOST memory: pinned host
+tensor (device generation + D2H inside the timed region, every step), and a
+pageable numpy array (the reference's own `fill(np.empty(n))` usage).
 
 --impl reference: the reference's algorithm on this box's host cores (the CPU
-oracle port of zigfast's fill_normal, oracle/zf_oracle.c, sharded over all
-host threads with the reference's derive_seed scheme, quality.py:121-126).
+oracle port of zigfast's fill_normal, oracle/zf_oracle.c: xoshiro256++ per
+thread, sharded over all host threads with the reference's derive_seed scheme,
+quality.py:121-126) on the same n and seed, each thread filling its share
+through a reused chunk buffer as the reference's run_quality does.
 """
 
 from __future__ import annotations
@@ -39,21 +47,32 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "samples/sec (fp64 normal & exponential) at 1/2/4/8 B200; % of HBM write roofline"
 UNIT = "samples/s"
-N_DEFAULT = 1 << 28
-SEED = 1234
+N_DEFAULT = 1 << 32          # config 3: 2^32 per GPU
+SEED = 7                     # config 3
+C2_N, C2_SEED = 1 << 28, 1234
+C5_TOTAL = 1 << 36           # config 5: 2^36 draws per distribution over all ranks
+E2E_N = 1 << 28              # bounded e2e sample per rank per step
+CPU_CHUNK = 1 << 20          # per-thread reused buffer of the CPU arms
+WORKLOAD = ("C3: N(0,1) fp64, n=2^32 per GPU per step, seed 7, counter-based substreams "
+            "(GPU g at counter g*2^40)")
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--n", type=int, default=N_DEFAULT)
-    p.add_argument("--cpu-seconds", type=float, default=8.0,
+    p.add_argument("--seed", type=int, default=SEED)
+    p.add_argument("--cpu-seconds", type=float, default=10.0,
                    help="target duration of the CPU baseline sample")
+    p.add_argument("--c5-total", type=int, default=C5_TOTAL)
+    p.add_argument("--e2e-n", type=int, default=E2E_N)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extra", action="store_true",
+                   help="headline leg only (no exp / aggregate / C2 / C5 legs)")
     return p.parse_args()
 
 
@@ -139,6 +158,7 @@ class ClockSampler:
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
         pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_min_mhz": min(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
 
@@ -148,36 +168,6 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
-
-
-def cpu_baseline(dist: str, seconds: float, threads: int | None = None):
-    """Time the reference algorithm (CPU oracle port) on `threads` host threads
-    for a bounded sample of roughly `seconds` of work."""
-    import numpy as np
-    from oracle import oracle
-    threads = threads or cpu_threads()
-    oracle.fill_sharded(dist, 1 << 16, 1, threads=threads)  # warm
-    n = max(threads << 18, 1 << 20)
-    while True:
-        buf = np.empty(n)
-        t0 = time.perf_counter()
-        oracle.fill_sharded(dist, n, SEED, threads=threads, out=buf)
-        dt = time.perf_counter() - t0
-        if dt >= seconds / 4 or n >= (1 << 31):
-            break
-        n = min(int(n * max(2.0, seconds / 4 / max(dt, 1e-3))), 1 << 31)
-    reps = max(1, int(round(seconds / max(dt, 1e-3))))
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        oracle.fill_sharded(dist, n, SEED, threads=threads, out=buf)
-        times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": n / statistics.median(times), "best": n / best, "unit": UNIT,
-            "cores": threads, "kind": "port",
-            "sample": f"{dist} fp64, {n} samples per rep x {reps} reps (median), sharded over "
-                      f"{threads} threads with derive_seed (quality.py:121-126), oracle/zf_oracle.c",
-            "cpu_model": _cpu_model()}
 
 
 def _cpu_model():
@@ -190,72 +180,71 @@ def _cpu_model():
     return None
 
 
+def _cpu_sample_desc(dist, n, threads):
+    return (f"{dist} fp64, n={n} per rep (the config's n per GPU), seed {SEED}, sharded over "
+            f"{threads} threads with derive_seed (quality.py:121-126), each thread filling "
+            f"its share through a reused {CPU_CHUNK}-sample buffer (run_quality's pattern); "
+            f"oracle/zf_oracle.c")
+
+
+def cpu_baseline(dist: str, n: int, seed: int, seconds: float, threads: int | None = None):
+    """The reference algorithm (CPU oracle port) on `threads` host threads on
+    the same n and seed as the GPU arm, repeated for about `seconds`."""
+    from oracle import oracle
+    threads = threads or cpu_threads()
+    oracle.fill_sharded_chunked(dist, 1 << 16, 1, threads=threads, chunk=CPU_CHUNK)  # warm
+    t0 = time.perf_counter()
+    oracle.fill_sharded_chunked(dist, n, seed, threads=threads, chunk=CPU_CHUNK)
+    times = [time.perf_counter() - t0]
+    while sum(times) < seconds and len(times) < 50:
+        t0 = time.perf_counter()
+        oracle.fill_sharded_chunked(dist, n, seed, threads=threads, chunk=CPU_CHUNK)
+        times.append(time.perf_counter() - t0)
+    return {"value": n / statistics.median(times), "best": n / min(times), "unit": UNIT,
+            "cores": threads, "kind": "port", "reps": len(times),
+            "sample": _cpu_sample_desc(dist, n, threads), "cpu_model": _cpu_model()}
+
+
 def run_reference(args, rank: int):
+    """The reference arm: the same workload (n, seed) on the host cores."""
     if rank != 0:
         return
-    threads = cpu_threads()
-    import numpy as np
     from oracle import oracle
-    n = max(threads << 22, 1 << 24)  # bounded per-step sample (~tens of ms of CPU work)
-    buf = np.empty(n)
+    threads = cpu_threads()
+    n = args.n
     for _ in range(args.warmup):
-        oracle.fill_sharded("normal", n, SEED, threads=threads, out=buf)
+        oracle.fill_sharded_chunked("normal", n, args.seed, threads=threads, chunk=CPU_CHUNK)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.fill_sharded("normal", n, SEED, threads=threads, out=buf)
+        oracle.fill_sharded_chunked("normal", n, args.seed, threads=threads, chunk=CPU_CHUNK)
     dt = time.perf_counter() - t0
     value = n * args.steps / dt
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded)", "impl": "reference",
-            "config": {"workload": "C2: N(0,1) fp64, seed 1234 (bounded CPU sample per step)",
-                       "n_per_step": n, "dist": "normal"},
+            "config": {"workload": WORKLOAD, "n_per_gpu": n, "dist": "normal",
+                       "seed": args.seed, "cpu_threads": threads},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{n} normal fp64 samples per step, {threads} threads, "
-                                       "derive_seed sharding, oracle/zf_oracle.c"},
+                             "sample": _cpu_sample_desc("normal", n, threads),
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def time_fill(sampler, out, steps: int, warmup: int, stream):
+def timed(fn, steps: int, warmup: int, stream, barrier=None):
+    """ms per step of fn() over `steps` calls, CUDA events on `stream`."""
     import torch
     for _ in range(warmup):
-        sampler.fill(out)
+        fn()
     torch.cuda.synchronize()
+    if barrier:
+        barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(steps):
-        sampler.fill(out)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    return t0.elapsed_time(t1) / steps  # ms per launch (one kernel per step)
-
-
-def time_aggregate(sampler, n: int, steps: int, warmup: int, stream):
-    """Device time of the fused generate-and-sum kernel (sum of n draws, no
-    HBM writes) -- the reference's own bench loop, `_kernels.py:703-922`."""
-    import ctypes as C
-
-    import torch
-    from paper_1403_6870_b200 import _lib, quality
-    cfg = quality._cfg(moments=1)
-    partials, counts = quality._buffers(sampler.device, n, cfg)
-    lib = _lib.lib()
-    src = sampler.source
-
-    def one():
-        _lib.check(lib.zf_fill_stats(sampler._dev_tables.handle, sampler._dist,
-                                     int(src.state[0]), int(src.state[1]), n, C.byref(cfg),
-                                     partials.data_ptr(), counts.data_ptr(), stream.cuda_stream))
-    for _ in range(warmup):
-        one()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(steps):
-        one()
+        fn()
     t1.record(stream)
     torch.cuda.synchronize()
     return t0.elapsed_time(t1) / steps
@@ -276,6 +265,20 @@ def write_peak(buf, reps: int = 10):
     return buf.numel() * buf.element_size() * reps / (t0.elapsed_time(t1) * 1e-3) / 1e9
 
 
+def profile_traffic(n: int):
+    """DRAM bytes per launch of the headline kernel from the committed ncu
+    capture of this configuration (profiles/), or None."""
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(prof.read_text())
+        rec = d.get("fill_normal_f64", {}).get(str(n))
+        if rec:
+            return rec["bytes_per_launch"], rec["source"]
+    except Exception:
+        pass
+    return None, None
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -284,133 +287,175 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if world > 1:  # lets the driver see the communicator's rank count in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_1403_6870_b200 as zf
-    from paper_1403_6870_b200 import quality, shard
+    from paper_1403_6870_b200 import scale, shard
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    barrier = dist.barrier if world > 1 else None
     n = args.n
     stream = torch.cuda.current_stream(dev)
     out = torch.empty(n, dtype=torch.float64, device=dev)
+    base = shard.counter_base(rank)
 
     def sampler(cls, s):
-        return cls(source=zf.UniformSource.counter(s, shard.counter_base(rank)), device=dev)
+        return cls(source=zf.UniformSource.counter(s, base), device=dev)
 
-    normal = sampler(zf.NormalSampler, SEED)
-    expo = sampler(zf.ExpSampler, SEED)
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
-    # exponential leg first (reported beside the headline)
-    exp_ms = time_fill(expo, out, args.steps, args.warmup, stream)
-    agg_ms = time_aggregate(normal, n, args.steps, args.warmup, stream)
-
-    # headline: normal, with clocks sampled during the timed region
-    for _ in range(args.warmup):
+    normal = sampler(zf.NormalSampler, args.seed)
+    expo = sampler(zf.ExpSampler, args.seed)
+    # every step refills the same counter range: sample k of this rank is
+    # global sample g*2^40 + k of seed 7 in every step (fill() of a sampler
+    # would advance the stream; the workload is the fixed config-3 range)
+    def fill_normal():
+        normal.source.state[1] = base
         normal.fill(out)
+
+    def fill_exp():
+        expo.source.state[1] = base
+        expo.fill(out)
+
+    # -- headline: first, on an idle GPU ------------------------------------------
+    fill_normal()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    time.sleep(1.0)  # let the power average settle after start-up before the timed leg
+    for _ in range(args.warmup):
+        fill_normal()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            normal.fill(out)
+            fill_normal()
         t1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    if barrier:
+        barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    ms_all = torch.tensor([ms, exp_ms, agg_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_all, op=dist.ReduceOp.MAX)
-    ms_max, exp_ms_max, agg_ms_max = ms_all.tolist()
+    (ms_max,) = max_over_ranks([ms])
+    # validation of the last headline step; only these sums cross NCCL
+    sums, hist, tails = scale.buffer_stats(out)
+    c3 = scale.validate_config3(sums, hist, tails, n, device=dev)
 
-    # validation of the last step's output; only these sums cross NCCL
-    sums, res = quality.buffer_sums(out, hist=(-6.0, 6.0, 1024), thresholds=(5.0, 6.0, 7.0),
-                                    abs_thresh=True)
-    # the only collective: a SUM allreduce of ~1 k validation numbers (NCCL)
-    stats_vec = torch.tensor(shard.allreduce_stats(
-        shard.pack_stats(sums, res.hist.tolist(), res.thresh_counts), device=dev),
-        dtype=torch.float64)
-    wp = write_peak(out) if rank == 0 else None
+    extra = {}
+    if not args.no_extra:
+        exp_ms = timed(fill_exp, args.steps, 2, stream, barrier)
+        from paper_1403_6870_b200 import quality
 
-    # e2e through the public API into pinned host memory (rank-local)
-    e2e = None
-    if not args.no_e2e:
-        host = torch.empty(n, dtype=torch.float64).pin_memory()
-        e2e_s = sampler(zf.NormalSampler, SEED + 1)
-        e2e_s.fill(host[: 1 << 20])
+        def agg():
+            normal.source.state[1] = base
+            quality.device_sums(normal, n, moments=1)
+        agg_ms = timed(agg, max(1, args.steps // 2), 2, stream, barrier)
+        # config 2 (validation leg): 2^28, seed 1234
+        c2s = zf.NormalSampler(source=zf.UniformSource.counter(C2_SEED, base), device=dev)
+        c2o = out[:C2_N]
+        c2s.fill(c2o)
+        s2, h2, t2 = scale.buffer_stats(c2o)
+        c2 = scale.validate_config3(s2, h2, t2, C2_N, device=dev)
+        # config 5 (tail stress): total draws per distribution over all ranks
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e_steps = max(1, min(args.steps, 3))
-        t = time.perf_counter()
-        for _ in range(e_steps):
-            e2e_s.fill(host)
+        if barrier:
+            barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c5 = scale.config5(args.c5_total, rank, world, device=dev)
+        e1.record(stream)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t
-        dt_t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
-        dt = dt_t.item()
-        e2e = {"value": n * world * e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": 8 * n, "steps": e_steps,
-               "note": "NormalSampler.fill(pinned host tensor): device generation + D2H copy, "
-                       "double-buffered 2^24-sample chunks; the input is a seed (no H2D bytes)"}
-
-    if rank == 0:
-        peak, peak_src = peaks()
-        achieved = 8 * n / (ms_max * 1e-3) / 1e9
-        v = stats_vec.tolist()
-        tot = n * world
-        raw = [s / tot for s in v[:4]]
-        mean, var, skew, exkurt = quality.central_moments_from_raw(raw)
-        hist = __import__("numpy").array(v[5:5 + 1026])
-        chi2, dof, chi2_z = quality.histogram_chi2(hist, tot, -6.0, 6.0)
-        traffic = None
-        prof = ROOT / "profiles" / "ncu_traffic.json"
-        if prof.exists():
-            try:
-                traffic = json.loads(prof.read_text()).get("fill_normal_f64_bytes_per_launch")
-            except Exception:
-                traffic = None
-        line = {
-            "metric": METRIC, "value": n * world / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded counter stream; no dataset)",
-            "config": {"workload": "C2: N(0,1) fp64, n=2^28 per GPU per step, seed 1234, "
-                                   "counter-based substreams (GPU g at counter g*2^40)",
-                       "n_per_gpu": n, "dist": "normal", "seed": SEED,
-                       "l2": "output 2 GiB per step > 126 MB L2 (no flush needed)",
-                       "parallelism": f"dp{world} (disjoint counter ranges, no hot-path collective)"},
+        exp_ms_max, agg_ms_max, c5_ms_max = max_over_ranks(
+            [exp_ms, agg_ms, e0.elapsed_time(e1)])
+        extra = {
             "exp_value": n * world / (exp_ms_max * 1e-3), "exp_ms_per_step": exp_ms_max,
             "aggregate": {"value": n * world / (agg_ms_max * 1e-3), "unit": UNIT,
                           "ms_per_step": agg_ms_max, "kernel": "fill_stats_kernel<normal,sum>",
                           "note": "generate-and-sum of the same n draws, nothing written "
                                   "(the reference's aggregate / bench loop)"},
+            "c2_validation": {"workload": "C2: N(0,1) fp64, n=2^28 per GPU, seed 1234", **c2},
+            "c5": {"workload": "C5: N(0,1) + Exp(1) fp64, generate-and-count, seed 99",
+                   "ms_max_over_ranks": c5_ms_max,
+                   "samples_per_s": 2 * args.c5_total / (c5_ms_max * 1e-3), **c5},
+        }
+    wp = write_peak(out[:1 << 28]) if rank == 0 else None
+
+    # -- e2e through the public API into host memory (rank-local) -------------------
+    e2e = None
+    if not args.no_e2e:
+        m = min(n, args.e2e_n)
+        host = torch.empty(m, dtype=torch.float64).pin_memory()
+        e2e_s = sampler(zf.NormalSampler, args.seed)
+        e2e_s.fill(host[: 1 << 20])
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_s.fill(host)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        arr = np.empty(m)
+        e2e_s.fill(arr[: 1 << 22])  # staging buffers allocated outside the timed region
+        p_steps = max(1, min(args.steps, 5))
+        if barrier:
+            barrier()
+        t = time.perf_counter()
+        for _ in range(p_steps):
+            e2e_s.fill(arr)
+        dtp = time.perf_counter() - t
+        dt, dtp = max_over_ranks([dt, dtp])
+        e2e = {"value": m * world * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": 8 * m, "steps": args.steps, "n_per_step": m,
+               "note": "NormalSampler.fill(pinned host tensor), every step: device generation + "
+                       "D2H copy of the step's 2^28 samples (double-buffered chunks); the input "
+                       "is a seed passed by value (no H2D bytes)",
+               "pageable": {"value": m * world * p_steps / dtp, "unit": UNIT, "steps": p_steps,
+                            "note": "NormalSampler.fill(np.empty(2^28)), the reference's own "
+                                    "usage (exponential.py:45-50): pinned staging + host copy"}}
+        del host
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = 8 * n / (ms_max * 1e-3) / 1e9
+        traffic, traffic_src = profile_traffic(n)
+        line = {
+            "metric": METRIC, "value": n * world / (ms_max * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter stream; no dataset)",
+            "config": {"workload": WORKLOAD, "n_per_gpu": n, "dist": "normal", "seed": args.seed,
+                       "counter_base": "rank * 2^40",
+                       "l2": "output 32 GiB per step >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"dp{world} (disjoint counter ranges, no hot-path "
+                                      "collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
                          "bytes_per_sample": 8, "write_peak_gbs": wp,
                          "frac_of_write_peak": achieved / wp if wp else None,
                          "kernel": "fill_ctr_kernel<normal,f64>"},
-            "validation": {"mean": mean, "var": var, "skew": skew, "excess_kurtosis": exkurt,
-                           "z": [mean / (1 / tot) ** 0.5, (var - 1) / (2 / tot) ** 0.5,
-                                 skew / (6 / tot) ** 0.5, exkurt / (24 / tot) ** 0.5],
-                           "hist_chi2": chi2, "hist_dof": dof, "hist_z": chi2_z,
-                           "tail_counts_abs_gt_5_6_7": v[5 + 1026:5 + 1029],
-                           "allreduce": "nccl" if world > 1 else "none"},
+            "validation": {**c3, "allreduce": "nccl" if world > 1 else "none"},
             "clocks": clk.summary(),
             "gpu_launches": args.steps,  # one fill_ctr_kernel launch per timed step
             "e2e": e2e,
+            **extra,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline("normal", args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline("normal", n, args.seed, args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

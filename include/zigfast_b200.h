@@ -9,6 +9,13 @@
  * default stream).  Every entry point returns 0 on success, a negative
  * ZF_E* code for invalid arguments, or a positive cudaError_t.
  *
+ * Devices: a table handle belongs to the device it was created on.  Calls that
+ * take a handle make that device current for their duration and restore the
+ * caller's current device before returning, so they work whichever device is
+ * current; their buffers and stream must belong to the handle's device.
+ * Calls without a handle (zf_stats, zf_words, zf_format_g17) run on the
+ * caller's current device.
+ *
  * Reference interfaces each entry point replaces (file:line under
  * /root/reference/pkg/src/zigfast/):
  *
@@ -129,8 +136,12 @@ typedef struct zf_stats_cfg {
   int32_t nbins;      /* 0 disables the histogram; counts has nbins + 2 slots (under, over) */
   int32_t nthresh;    /* <= 8 */
   int32_t abs_thresh; /* count |x| > t instead of x > t */
-  int32_t moments;    /* 0 or 5: x^1..x^5; 1 with no histogram/thresholds: the
-                         sum only (aggregate, _kernels.py:306-393) */
+  int32_t moments;    /* 5: x^1..x^5; 1 with no histogram/thresholds: the sum
+                         only (aggregate, _kernels.py:306-393); 0: no moments
+                         (partials are zero) -- histogram / threshold counts
+                         only, and thresholds at or above every fast-path
+                         value of the table (e.g. |x| > 5 for N(0,1), x > X[1]
+                         for Exp(1)) are then counted on the rare path alone */
   double thresh[8];
 } zf_stats_cfg;
 

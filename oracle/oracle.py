@@ -63,6 +63,10 @@ def lib():
         L.orc_build_alias_vose.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_aggregate.restype = C.c_double
         L.orc_aggregate.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, u64p, C.c_uint64]
+        L.orc_fill_sharded_chunked.restype = C.c_int
+        L.orc_fill_sharded_chunked.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                               C.c_uint64, C.c_int, C.c_uint64,
+                                               C.POINTER(C.c_double)]
         L.orc_fill_sharded.restype = C.c_int
         L.orc_fill_sharded.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                        C.c_uint64, C.c_int]
@@ -267,3 +271,16 @@ def fill_sharded(dist, n: int, seed: int, threads: int | None = None,
                                 _ptr(out), n, threads)
     assert rc == 0
     return out
+
+
+def fill_sharded_chunked(dist, n: int, seed: int, threads: int | None = None,
+                         chunk: int = 1 << 20) -> float:
+    """`fill_sharded` through one reused `chunk`-sample buffer per thread (the
+    reference's run_quality fill pattern); returns a checksum."""
+    h, e = packs(dist)
+    threads = threads or len(os.sched_getaffinity(0))
+    cs = C.c_double()
+    rc = lib().orc_fill_sharded_chunked(_dist(dist), C.byref(h.c), C.byref(e.c),
+                                        seed & (2**64 - 1), n, threads, chunk, C.byref(cs))
+    assert rc == 0
+    return cs.value

@@ -35,7 +35,6 @@ import numpy as np
 
 from .errors import CurvatureViolation, InvalidSpec, NonConvergence, QuadratureFailure
 from .tables import EXPONENTIAL, HALF_NORMAL, ZigguratTables
-from .traditional import _bisect_to_ulp
 
 _X0_FACTOR = 2.0  # x[0] is a finite placeholder, twice the tail start (never sampled)
 
@@ -72,6 +71,29 @@ def get(kind: str) -> DensitySpec:
     if kind == HALF_NORMAL:
         return half_normal()
     raise ValueError(f"unknown density kind: {kind!r}")
+
+
+def _bisect_to_ulp(fn, lo: float, hi: float) -> float:
+    """Bisection until the bracket has no representable midpoint
+    (`tables.py:107-127`)."""
+    flo, fhi = fn(lo), fn(hi)
+    if flo == 0.0:
+        return lo
+    if fhi == 0.0:
+        return hi
+    if (flo > 0.0) == (fhi > 0.0):
+        raise NonConvergence(f"no sign change on [{lo!r}, {hi!r}]")
+    while True:
+        mid = 0.5 * (lo + hi)
+        if mid <= lo or mid >= hi:
+            return hi if abs(fhi) < abs(flo) else lo
+        fmid = fn(mid)
+        if fmid == 0.0:
+            return mid
+        if (fmid > 0.0) == (flo > 0.0):
+            lo, flo = mid, fmid
+        else:
+            hi, fhi = mid, fmid
 
 
 def _right_root(gap, hi: float) -> float | None:

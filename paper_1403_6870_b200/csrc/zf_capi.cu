@@ -192,6 +192,7 @@ int zf_trad_tables_create_default(int device, zf_tables** out) {
 
 int zf_tables_destroy(zf_tables* t) {
   if (!t) return ZF_OK;
+  ZF_ON_DEVICE(t);
   cudaError_t e = cudaFree(t->dev);
   for (auto& sl : t->stage.slot) {
     if (sl.done) cudaEventSynchronize(sl.done), cudaEventDestroy(sl.done);
@@ -210,6 +211,7 @@ int zf_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr
   if (ctr_base > kMaxCtr || n > kMaxCtr - ctr_base) return ZF_ERANGE;
   const size_t esz = dtype == ZF_F32 ? 4 : 8;
   if (reinterpret_cast<uintptr_t>(out_dev) % esz) return ZF_EALIGN;
+  ZF_ON_DEVICE(t);
   return launch_fill(t, dist, dtype, seed, ctr_base, out_dev, n, counters_dev, as_stream(stream));
 }
 
@@ -218,6 +220,7 @@ int zf_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_base
                   void* stream) {
   if (!t || !partials_dev || !counts_dev) return ZF_EINVAL;
   if (ctr_base > kMaxCtr || n > kMaxCtr - ctr_base) return ZF_ERANGE;
+  ZF_ON_DEVICE(t);
   return launch_fill_stats(t, dist, seed, ctr_base, n, cfg, partials_dev, counts_dev,
                            as_stream(stream));
 }
@@ -235,6 +238,7 @@ int zf_fill_replay(const zf_tables* t, int dist, int dtype, const uint64_t* word
                    zf_path_rec* recs_dev, int64_t* counters_dev, uint64_t* words_consumed,
                    void* stream) {
   if (!t || !words_consumed) return ZF_EINVAL;
+  ZF_ON_DEVICE(t);
   return run_replay(t, dist, dtype, words_dev, nwords, cursor, wrap, out_dev, n, recs_dev,
                     counters_dev, words_consumed, as_stream(stream));
 }
@@ -268,6 +272,7 @@ int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* stat
                 const uint64_t* replay_words_dev, uint64_t nwords, void* out_dev, uint64_t n,
                 zf_path_rec* recs_dev, int64_t* counters_dev, void* stream) {
   if (!t || !state) return ZF_EINVAL;
+  ZF_ON_DEVICE(t);
   cudaStream_t s = as_stream(stream);
   if (gid == ZF_GEN_CTR) {
     if (recs_dev) return ZF_EINVAL;  // production mode has no stream positions
@@ -331,6 +336,7 @@ int zf_format_g17(const double* x_dev, uint64_t n, char* out_dev, uint64_t cap,
 int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                   void* out_dev, void* stream) {
   if (!t || (nreq > 0 && (!reqs || !out_dev))) return ZF_EINVAL;
+  ZF_ON_DEVICE(t);
   return launch_fill_batch(t, reqs, nreq, dtype, out_dev, as_stream(stream));
 }
 

@@ -274,13 +274,20 @@ __device__ __forceinline__ bool less_than_exp(double y, double arg) {
   return y < exp(arg);
 }
 
+// alias pick (_kernels.py:128-136) from its two words
+__device__ __forceinline__ int alias_from(const DevPack& p, uint64_t w1, uint64_t w2) {
+  const int n = p.nslots;
+  long long k = __double2ll_rz(__dmul_rn(u01(w1), (double)n));
+  if (k >= n) k = n - 1;
+  const double up = u01(w2);
+  return up < p.prob[k] ? (int)k : p.alias[k];
+}
+
 template <class S>
 __device__ __forceinline__ int alias_pick(const DevPack& p, S& s) {
-  const int n = p.nslots;
-  long long k = __double2ll_rz(__dmul_rn(u01(s.next()), (double)n));
-  if (k >= n) k = n - 1;
-  const double up = u01(s.next());
-  return up < p.prob[k] ? (int)k : p.alias[k];
+  const uint64_t w1 = s.next();
+  const uint64_t w2 = s.next();
+  return alias_from(p, w1, w2);
 }
 
 // Exponential draw whose first byte word `u` has already been taken from the
@@ -331,15 +338,67 @@ __device__ double exp_draw(const DevPack& p, uint64_t u, S& s, C& c, double shif
   }
 }
 
+// One attempt of the exponential box loop (_kernels.py:163-180) for slot j
+// from its two words: true and the value (shift + x) if accepted.
+__device__ __forceinline__ bool exp_box_words(const DevPack& p, int j, uint64_t wa, uint64_t wb,
+                                              double shift, double& v) {
+  double ux = u01(wa);
+  double uy = u01(wb);
+  if (ux > __dsub_rn(1.0, uy)) {
+    const double t = ux;
+    ux = __dsub_rn(1.0, uy);
+    uy = __dsub_rn(1.0, t);
+  }
+  if (uy < __dsub_rn(__dsub_rn(1.0, ux), p.eps)) {
+    v = __dadd_rn(__dadd_rn(shift, p.xlo[j]), __dmul_rn(ux, p.xw[j]));
+    return true;
+  }
+  const double x = __dadd_rn(p.xlo[j], __dmul_rn(ux, p.xw[j]));
+  const double y = __dadd_rn(p.flo[j], __dmul_rn(uy, p.fh[j]));
+  v = __dadd_rn(shift, x);
+  return less_than_exp(y, -x);
+}
+
+// Production exponential draw of an exceptional first word (exp_draw with
+// u = an exceptional byte) on the secondary counter stream at `sbase`: the
+// four words of the alias pick and the first box attempt are independent
+// counter positions, so they are computed side by side instead of one
+// dependent mix13 chain after another.  Same words, same arithmetic, same
+// value as exp_draw.
+__device__ __forceinline__ double exp_draw_ctr(const DevPack& p, uint64_t sbase) {
+  const uint64_t w1 = mix13(sbase + kGamma), w2 = mix13(sbase + 2 * kGamma);
+  const uint64_t w3 = mix13(sbase + 3 * kGamma), w4 = mix13(sbase + 4 * kGamma);
+  const int j = alias_from(p, w1, w2);
+  NoCount c;
+  if (j == 0) {  // tail: shift by X[1], word 3 is the next first word
+    CtrStream s{sbase + 3 * kGamma};
+    return exp_draw(p, w3, s, c, p.tailx);
+  }
+  double v;
+  if (exp_box_words(p, j, w3, w4, 0.0, v)) return v;
+  CtrStream s{sbase + 4 * kGamma};
+  for (;;) {
+    const uint64_t wa = s.next();
+    const uint64_t wb = s.next();
+    if (exp_box_words(p, j, wa, wb, 0.0, v)) return v;
+  }
+}
+
 // One attempt of the normal overhang box loop (_kernels.py:679-688) for slot j
 // from the stream's current position: true and x if accepted.
-template <class S>
-__device__ __forceinline__ bool normal_box_attempt(const DevPack& h, int j, S& s, double& x) {
-  const double ux = u01(s.next());
-  const double uy = u01(s.next());
+__device__ __forceinline__ bool normal_box_words(const DevPack& h, int j, uint64_t wa, uint64_t wb,
+                                                 double& x) {
+  const double ux = u01(wa);
+  const double uy = u01(wb);
   x = __dadd_rn(h.xlo[j], __dmul_rn(ux, h.xw[j]));
   const double y = __dadd_rn(h.flo[j], __dmul_rn(uy, h.fh[j]));
   return less_than_exp(y, __dmul_rn(__dmul_rn(-0.5, x), x));
+}
+template <class S>
+__device__ __forceinline__ bool normal_box_attempt(const DevPack& h, int j, S& s, double& x) {
+  const uint64_t wa = s.next();
+  const uint64_t wb = s.next();
+  return normal_box_words(h, j, wa, wb, x);
 }
 
 // Normal tail beyond r = X[1] (_kernels.py:611-678): Marsaglia's method with
@@ -528,6 +587,58 @@ __device__ __forceinline__ void stage_block(void* dst, const void* src, int byte
   int4* d = reinterpret_cast<int4*>(dst);
   const int4* g = reinterpret_cast<const int4*>(src);
   for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) d[i] = __ldg(g + i);
+}
+
+// ---------------------------------------------------------------------------
+// asynchronous staging (TMA bulk copies completing on shared-memory mbarriers)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+// one thread: expect `bytes` on `bar` and start the bulk copy global -> shared
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Stage a table image whose first `head` bytes pass 1 needs at once (the
+// fast-path scale array) and whose remaining `bytes - head` only the rare
+// rounds read: thread 0 starts two bulk copies; the block waits for the head
+// here, each warp waits for the tail (bars[1], phase 0) before its first
+// round.  Call from every thread; includes a __syncthreads.
+__device__ __forceinline__ void stage_split(void* dst, const void* src, int head, int bytes,
+                                            uint64_t* bars) {
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bulk_load(dst, src, (uint32_t)head, &bars[0]);
+    bulk_load(static_cast<char*>(dst) + head, static_cast<const char*>(src) + head,
+              (uint32_t)(bytes - head), &bars[1]);
+  }
+  __syncthreads();
+  mbar_wait(&bars[0], 0);
 }
 
 }  // namespace zf

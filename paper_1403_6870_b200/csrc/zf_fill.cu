@@ -47,11 +47,25 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kPacks = kPacksOf<DIST>;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
-  stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   const int lane = threadIdx.x & 31;
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kPacks * sizeof(DevPack)) +
                     (threadIdx.x >> 5) * kQueueWords;
+  const uint64_t* late = nullptr;
+#if ZF_ASYNC_STAGE
+  __shared__ uint64_t bars[2];
+  if constexpr (!kTrad<DIST>) {
+    // pass 1 reads only sx; everything after it is for the rounds
+    stage_split(sp, primary_pack<DIST>(gt), (int)sizeof(sp->sx), kPacks * (int)sizeof(DevPack),
+                bars);
+    late = &bars[1];
+  } else {
+    stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
+    __syncthreads();
+  }
+#else
+  stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   __syncthreads();
+#endif
   const DevPack& P = sp[0];
   const DevPack& E = sp[kPacks - 1];
 
@@ -59,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
   StoreSink<OutT, VEC> sink{out};
   run_tiles<DIST, COUNTED, P2>(P, E, seed, ctr_base, sink, n,
                                (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
-                               (uint64_t)gridDim.x * kWarps, queue, lane, lc);
+                               (uint64_t)gridDim.x * kWarps, queue, lane, lc, late);
   if (COUNTED) flush_counts(lc, counters);
 }
 
@@ -262,10 +276,7 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
   BatchStage& sl = t->stage.slot[t->stage.next];
   t->stage.next = (t->stage.next + 1) % kStageSlots;
   if (sl.done) ZF_TRY(cudaEventSynchronize(sl.done));  // its previous batch has read it
-  if (sl.cap < bytes || !sl.done) {  // (re)allocate on the handle's device
-    int prev = 0;
-    ZF_TRY(cudaGetDevice(&prev));
-    ZF_TRY(cudaSetDevice(t->device));
+  if (sl.cap < bytes || !sl.done) {  // (re)allocate; the caller made t->device current
     cudaError_t e = cudaSuccess;
     if (sl.cap < bytes) {
       const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
@@ -279,7 +290,6 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
       if (e == cudaSuccess) sl.cap = cap;
     }
     if (e == cudaSuccess && !sl.done) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
-    cudaSetDevice(prev);
     ZF_TRY(e);
   }
   uint32_t* cmap = reinterpret_cast<uint32_t*>(sl.host + req_bytes);

@@ -50,6 +50,32 @@ inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? ZF_OK : (int)e
     if (_s != ZF_OK) return _s;                     \
   } while (0)
 
+// Makes the handle's device current for the scope of a call and restores the
+// caller's device afterwards, so a handle works whatever device is current.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev_) == cudaSuccess && prev_ != device) {
+      status_ = cudaSetDevice(device);
+      switched_ = status_ == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (switched_) cudaSetDevice(prev_);
+  }
+  cudaError_t status() const { return status_; }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+ private:
+  int prev_ = -1;
+  bool switched_ = false;
+  cudaError_t status_ = cudaSuccess;
+};
+#define ZF_ON_DEVICE(t)                               \
+  zf::DeviceGuard zf_guard_((t)->device);             \
+  if (zf_guard_.status() != cudaSuccess) return (int)zf_guard_.status()
+
 constexpr uint64_t kMaxCtr = 1ull << 44;  // primary counter range (see zf_device.cuh)
 
 constexpr int kKindModified = 0;

@@ -32,8 +32,8 @@ struct StatsShared {
 // the per-warp queues (and their 16-byte round scratch) follow it
 static_assert(sizeof(StatsShared) % 16 == 0, "queue alignment");
 
-template <bool EXTRA>
-__device__ void init_sink(StatsSinkT<EXTRA>& k, StatsShared* sh, unsigned int* hist,
+template <bool EXTRA, bool MOMENTS>
+__device__ void init_sink(StatsSinkT<EXTRA, MOMENTS>& k, StatsShared* sh, unsigned int* hist,
                           const zf_stats_cfg& cfg) {
   if (cfg.nbins)  // hist has nbins + 2 slots only when the histogram is enabled
     for (int i = threadIdx.x; i < cfg.nbins + 2; i += blockDim.x) hist[i] = 0;
@@ -53,8 +53,9 @@ __device__ void init_sink(StatsSinkT<EXTRA>& k, StatsShared* sh, unsigned int* h
     if (q < cfg.nthresh) k.tmin = fmin(k.tmin, cfg.thresh[q]);
 }
 
-template <bool EXTRA>
-__device__ void flush_sink(const StatsSinkT<EXTRA>& k, StatsShared* sh, const unsigned int* hist,
+template <bool EXTRA, bool MOMENTS>
+__device__ void flush_sink(const StatsSinkT<EXTRA, MOMENTS>& k, StatsShared* sh,
+                           const unsigned int* hist,
                            const zf_stats_cfg& cfg, double* __restrict__ partials,
                            unsigned long long* __restrict__ counts) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -98,8 +99,25 @@ __device__ void flush_sum(double v, StatsShared* sh, double* __restrict__ partia
   }
 }
 
+// Tail-only flush: threshold counts (atomics), zero partial rows.
+__device__ void flush_tail(const TailSink& k, const zf_stats_cfg& cfg,
+                           double* __restrict__ partials, unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q >= cfg.nthresh) break;
+    unsigned long long v = k.thr[q];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0 && v) atomicAdd(counts + cfg.nbins + 2 + q, v);
+  }
+  if (threadIdx.x < 5) partials[(uint64_t)blockIdx.x * 5 + threadIdx.x] = 0.0;
+}
+
 // MODE 0: the aggregate (moments == 1, no histogram, no thresholds);
-// 1: moments x^1..x^5 only; 2: moments + histogram + threshold counts.
+// 1: moments x^1..x^5 only; 2: moments + histogram + threshold counts;
+// 3: histogram / threshold counts without moments (moments == 0);
+// 4: threshold counts above every fast-path value (see TailSink).
 template <int DIST, int MODE>
 __global__ void __launch_bounds__(kThreads)
     fill_stats_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
@@ -123,8 +141,20 @@ __global__ void __launch_bounds__(kThreads)
     run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
                               queue, lane, lc);
     flush_sum(sink.s, sh, partials);
+  } else if constexpr (MODE == 4) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (threadIdx.x == q) sh->thresh[q] = cfg.thresh[q];
+    TailSink sink;
+    sink.nthresh = cfg.nthresh;
+    sink.abs_t = cfg.abs_thresh != 0;
+    sink.t = sh->thresh;
+    __syncthreads();
+    run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
+                              queue, lane, lc);
+    flush_tail(sink, cfg, partials, counts);
   } else {
-    StatsSinkT<MODE == 2> sink;
+    StatsSinkT<MODE == 2 || MODE == 3, MODE != 3> sink;
     init_sink(sink, sh, hist, cfg);
     __syncthreads();
     run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
@@ -178,6 +208,21 @@ int check_cfg(const zf_stats_cfg* cfg) {
 bool extra(const zf_stats_cfg* cfg) { return cfg->nbins != 0 || cfg->nthresh != 0; }
 bool sum_only(const zf_stats_cfg* cfg) { return cfg->moments == 1 && !extra(cfg); }
 
+// Every threshold at or above the largest fast-path magnitude of the
+// (modified) table: fast x = u * sx[i + 1], i < lmax, |u| <= 2^64 (exp) or
+// 2^63 (normal), so |x| <= max sx * 2^64 (2^63) exactly (power-of-two scale).
+bool tail_only(const zf_tables* t, int dist, const zf_stats_cfg* cfg) {
+  if (cfg->nbins != 0 || cfg->nthresh == 0 || t->kind != kKindModified) return false;
+  if (dist != ZF_EXP && dist != ZF_NORMAL) return false;
+  const DevPack& p = dist == ZF_EXP ? t->host.ex : t->host.hn;
+  double m = 0.0;
+  for (int i = 1; i <= p.lmax; ++i) m = std::max(m, p.sx[i]);
+  const double fast_max = m * (dist == ZF_EXP ? 0x1p64 : 0x1p63);
+  for (int q = 0; q < cfg->nthresh; ++q)
+    if (!(cfg->thresh[q] >= fast_max)) return false;
+  return true;
+}
+
 size_t hist_bytes(const zf_stats_cfg* cfg) {
   return cfg->nbins ? ((size_t)(cfg->nbins + 2) * sizeof(unsigned int) + 15) / 16 * 16 : 0;
 }
@@ -189,12 +234,17 @@ int launch_fill_stats_dist(const zf_tables* t, uint64_t seed, uint64_t ctr_base,
                            cudaStream_t s) {
   constexpr int kPacks = kPacksOf<DIST>;
   const uint32_t grid = stats_blocks(n);
-  const int mode = sum_only(cfg) ? 0 : extra(cfg) ? 2 : 1;
+  const int mode = sum_only(cfg)                    ? 0
+                   : cfg->moments != 0               ? (extra(cfg) ? 2 : 1)
+                   : tail_only(t, DIST, cfg)         ? 4
+                                                     : 3;
   const size_t smem = kPacks * sizeof(DevPack) + sizeof(StatsShared) +
                       (size_t)kWarps * kQueueWords * sizeof(uint32_t) + hist_bytes(cfg);
   auto kern = mode == 0   ? fill_stats_kernel<DIST, 0>
               : mode == 1 ? fill_stats_kernel<DIST, 1>
-                          : fill_stats_kernel<DIST, 2>;
+              : mode == 2 ? fill_stats_kernel<DIST, 2>
+              : mode == 3 ? fill_stats_kernel<DIST, 3>
+                          : fill_stats_kernel<DIST, 4>;
   ZF_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, n, *cfg, partials, counts);
   return cuda_status(cudaGetLastError());

@@ -35,6 +35,15 @@ static_assert((1 << kTileBits) == kTile, "tile must be 256, 512 or 1024 samples"
 #endif
 constexpr int kPass1Unroll = ZF_PASS1_UNROLL;
 
+// Rounds compute the alias-pick and first-attempt words side by side.
+#ifndef ZF_HOIST
+#define ZF_HOIST 0
+#endif
+// Tables staged by two bulk copies: pass 1 waits only for the scale array.
+#ifndef ZF_ASYNC_STAGE
+#define ZF_ASYNC_STAGE 0
+#endif
+
 #ifndef ZF_QUEUE_CAP
 #define ZF_QUEUE_CAP 128
 #endif
@@ -115,7 +124,9 @@ struct SumSink {
 
 // Validation statistics: raw power sums x^1..x^5 (quality.py:92-106), an
 // equal-width histogram with under/overflow bins and threshold counts.
-template <bool EXTRA>  // false: moments only (no histogram / thresholds)
+// EXTRA = false: moments only (no histogram / thresholds); MOMENTS = false:
+// histogram / thresholds only.
+template <bool EXTRA, bool MOMENTS = true>
 struct StatsSinkT {
   using Out = double;
   static constexpr int V = 2;
@@ -127,16 +138,18 @@ struct StatsSinkT {
   bool abs_t;
   const double* t;  // thresholds (smem)
   __device__ __forceinline__ void add(double x) {
-    double p = x;
-    s[0] += p;
-    p *= x;
-    s[1] += p;
-    p *= x;
-    s[2] += p;
-    p *= x;
-    s[3] += p;
-    p *= x;
-    s[4] += p;
+    if constexpr (MOMENTS) {
+      double p = x;
+      s[0] += p;
+      p *= x;
+      s[1] += p;
+      p *= x;
+      s[2] += p;
+      p *= x;
+      s[3] += p;
+      p *= x;
+      s[4] += p;
+    }
     if constexpr (EXTRA) {
       const double a = abs_t ? fabs(x) : x;
       if (a > tmin) {  // tail counts: almost every sample is below all thresholds
@@ -164,6 +177,31 @@ struct StatsSinkT {
   }
 };
 using StatsSink = StatsSinkT<true>;
+
+// Tail counts only, for thresholds no fast-path value can exceed (every one
+// at or above the table's largest fast-path magnitude, e.g. |x| > 5, 6, 7 and
+// x > X[1] in config 5): pass 1 only flags exceptional samples, and just the
+// values that come out of the rounds (and the ragged last tile) are compared.
+struct TailSink {
+  using Out = double;
+  static constexpr int V = 2;
+  // per-lane counts: a lane sees < 2^32 samples (2^44 / the stats grid's threads)
+  uint32_t thr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int nthresh;
+  bool abs_t;
+  const double* t;  // thresholds (smem)
+  __device__ __forceinline__ void flag(uint32_t& mask, double d, uint32_t bit) {
+    or_if_nan(mask, d, bit);
+  }
+  __device__ __forceinline__ void put_vec(uint64_t, const double*, uint32_t) {}
+  __device__ __forceinline__ void put(uint64_t, double x, bool exc) {
+    if (exc) return;
+    const double a = abs_t ? fabs(x) : x;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < nthresh) thr[q] += a > t[q];
+  }
+};
 
 
 // Pass 1 of one warp tile: samples [base, min(base + kTile, n)) of the counter
@@ -243,6 +281,13 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
   return;
 #endif
   const uint64_t K = ctr_base + k;
+#if ZF_HOIST
+  if constexpr (DIST == ZF_EXP && !COUNTED) {
+    sink.put(k, to_out<OutT>(exp_draw_ctr(P, seed + (kExcBase + (K << kExcShift)) * kGamma)),
+             false);
+    return;
+  }
+#endif
   // k is exceptional: the modified exponential draw only needs to know that
   // (its first word's bits are never read again), the normal one needs the
   // sign bit, the traditional ones the whole word
@@ -293,10 +338,25 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
   const uint64_t K = ctr_base + k;
   const uint64_t u = mix13(seed + (K + 1) * kGamma);  // the sign word
   const uint64_t sbase = seed + (kExcBase + (K << kExcShift)) * kGamma;
-  CtrStream s{sbase};
-  const int j = alias_pick(P, s);
   double val;
   bool done;
+#if ZF_HOIST
+  // the alias pick's and the first box attempt's words are independent
+  // counter positions: compute them side by side
+  const uint64_t w1 = mix13(sbase + kGamma), w2 = mix13(sbase + 2 * kGamma);
+  const uint64_t w3 = mix13(sbase + 3 * kGamma), w4 = mix13(sbase + 4 * kGamma);
+  const int j = alias_from(P, w1, w2);
+  if (j == 0) {
+    NoCount c;
+    CtrStream s{sbase + 2 * kGamma};
+    val = normal_tail(P, E, s, c);
+    done = true;
+  } else {
+    done = normal_box_words(P, j, w3, w4, val);
+  }
+#else
+  CtrStream s{sbase};
+  const int j = alias_pick(P, s);
   if (j == 0) {
     NoCount c;
     val = normal_tail(P, E, s, c);
@@ -304,6 +364,7 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
   } else {
     done = normal_box_attempt(P, j, s, val);
   }
+#endif
   uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t un = __ballot_sync(0xffffffffu, !done); un;
@@ -381,6 +442,12 @@ __device__ __forceinline__ int warp_excl_mask(uint32_t mask, int lane, int* tota
   return __popc(any & ((1u << lane) - 1u));
 }
 
+// x without its highest set bit; 0 for x == 0 (the shift count is masked so
+// it stays defined when __clz(0) == 32)
+__device__ __forceinline__ uint32_t drop_top(uint32_t x) {
+  return x & ~(0x80000000u >> (__clz(x) & 31));
+}
+
 template <int V>
 __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
   return (uint32_t)((b / V) * 32 * V + lane * V + (b % V));
@@ -402,8 +469,17 @@ template <int DIST, bool COUNTED, int P2, class Sink>
 __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
                                           uint64_t first_tile, uint64_t stride, uint32_t* q,
-                                          int lane, LaneCounts& lc) {
+                                          int lane, LaneCounts& lc,
+                                          const uint64_t* late = nullptr) {
   static_assert(P2 == 3 || P2 == 9, "unknown pass-2 policy");
+  // `late`: mbarrier (phase 0) of the table arrays only the rounds read
+  bool tables_ready = late == nullptr;
+  auto need_tables = [&]() {
+    if (!tables_ready) {
+      mbar_wait(late, 0);
+      tables_ready = true;
+    }
+  };
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   // queue entry = tile iteration << kTileBits | lane * kPerLane | mask bit: the
   // enqueue loop (a few lanes active) only ORs the bit in; the full-warp
@@ -435,6 +511,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       if (qn + total > kQueueCap) {
         // (practically never: ~100 exceptions in one tile, expected ~15) resolve
         // this tile's exceptions in place, each lane walking its own mask
+        need_tables();
         for (uint32_t m = mask; m; m &= m - 1)
           resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink,
                                      tile * kTile + mask_bit_offset<Sink::V>(__ffs(m) - 1, lane),
@@ -458,7 +535,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
           // tiles): the second entry is predicated as well and the loop runs
           // only for lanes with three or more.  (The normal kernel loses 6 %
           // with it: +4 registers and a worse layout.)
-          const uint32_t m2 = mask & ~(0x80000000u >> __clz(mask));
+          const uint32_t m2 = drop_top(mask);
           const int hb2 = 31 - __clz(m2);
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
                        "@p st.shared.u32 [%0], %1;\n\t}"
@@ -466,7 +543,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                        : "memory");
           if (__ballot_sync(0xffffffffu, (m2 & (m2 - 1u)) != 0u)) {
             slot += 2;
-            for (uint32_t m = m2 & ~(0x80000000u >> __clz(m2)); m;) {
+            for (uint32_t m = drop_top(m2); m;) {
               const int b = 31 - __clz(m);
               m ^= 1u << b;
               q[slot++] = tag | (uint32_t)b;
@@ -474,7 +551,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
           }
           } else {
           ++slot;
-          for (uint32_t m = mask & ~(0x80000000u >> __clz(mask)); m;) {
+          for (uint32_t m = drop_top(mask); m;) {
             const int b = 31 - __clz(m);
             m ^= 1u << b;
             q[slot++] = tag | (uint32_t)b;
@@ -489,6 +566,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       continue;
 #endif
       if (qn < 32) continue;
+      need_tables();
       int done = 0;
       for (; qn - done >= 32; done += 32)
       {
@@ -505,6 +583,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       qn -= done;
       __syncwarp();
     }
+    if (qn) need_tables();
     if (lane < qn) resolve_one<DIST, COUNTED>(P, E, seed, ctr_base, sink, k_of(q[lane]), lc);
     __syncwarp();
   }

@@ -44,11 +44,15 @@ class StatsResult:
 
 
 def _cfg(hist=None, thresholds=(), abs_thresh=False, moments=5) -> _lib.StatsCfg:
-    if not 1 <= moments <= 5:
-        raise ValueError("moments must be in 1..5")
+    if not 0 <= moments <= 5:
+        raise ValueError("moments must be in 0..5")
+    if moments == 0 and hist is None and not thresholds:
+        raise ValueError("nothing to compute: no moments, histogram or thresholds")
     cfg = _lib.StatsCfg()
-    # 1 moment with no histogram / thresholds selects the sum-only kernel
-    cfg.moments = 1 if moments == 1 else 5
+    # 1 moment with no histogram / thresholds selects the sum-only kernel; 0
+    # moments with thresholds above every fast-path value the rare-path-only
+    # tail counter (zigfast_b200.h, zf_stats_cfg.moments)
+    cfg.moments = moments if moments <= 1 else 5
     if hist is not None:
         cfg.hist_lo, cfg.hist_hi, cfg.nbins = float(hist[0]), float(hist[1]), int(hist[2])
     if len(thresholds) > 8:
@@ -150,7 +154,9 @@ class QualityReport:
         return "\n".join(lines)
 
 
-def make_sampler(dist: str, seed, generator: str = "ctr", device=None):
+def make_sampler(dist: str, seed, generator: str = "xoshiro256++", device=None):
+    """`quality.make_sampler` (quality.py:83-89); ``generator`` defaults to the
+    reference's own stream, "ctr" selects the production counter stream."""
     from .samplers import ExpSampler, NormalSampler
     from .uniform import UniformSource
     source = UniformSource(seed, generator=generator)
@@ -161,32 +167,56 @@ def make_sampler(dist: str, seed, generator: str = "ctr", device=None):
     raise ValueError(f"unknown distribution: {dist!r}")
 
 
-def run_quality(dist: str, n: int, seed=None, jobs: int = 1, chunk: int = 1 << 22,
-                generator: str = "ctr", device=None) -> QualityReport:
-    """First five raw moments of ``n`` draws vs their analytic values
-    (`quality.py:109-138`).  ``jobs`` is accepted for API parity: one GPU
-    launch already spans every SM, so sharding is by counter range instead."""
+def _moment_sums(sampler, n: int, chunk: int) -> list[list[float]]:
+    """Per-chunk power sums of ``n`` draws (quality.py:92-106): the sampler
+    fills one reused device chunk at a time, exactly as the reference fills
+    views of one host buffer, so the stream is consumed identically; each
+    chunk is reduced on the device."""
     import torch
+    sums: list[list[float]] = [[] for _ in range(5)]
+    if sampler.source.gid == _lib.GEN_CTR:  # production: fused, nothing stored
+        s, _ = device_sums(sampler, n)
+        for k in range(5):
+            sums[k].append(s[k])
+        return sums
+    buf = torch.empty(min(chunk, n), dtype=torch.float64, device=sampler.device)
+    left = n
+    while left > 0:
+        m = min(chunk, left)
+        view = buf[:m]
+        sampler.fill(view)
+        s, _ = buffer_sums(view)
+        for k in range(5):
+            sums[k].append(s[k])
+        left -= m
+    return sums
+
+
+def run_quality(dist: str, n: int, seed=None, jobs: int = 1, chunk: int = 1 << 22,
+                generator: str = "xoshiro256++", device=None) -> QualityReport:
+    """First five raw moments of ``n`` draws vs their analytic values
+    (`quality.py:109-138`): ``jobs`` shards seeded ``derive_seed(base, i)``
+    with the reference's share split, every shard consuming its stream as the
+    reference does, per-chunk sums merged with ``math.fsum``.  The shards run
+    one after another (each fill already spans every SM).  The draws are the
+    reference's bit for bit; the per-chunk sums are fsum-exact rather than
+    numpy's pairwise order (|difference| ~1e-16 relative per chunk)."""
+    from .uniform import UniformSource, derive_seed
     if dist not in EXPECTED_MOMENTS:
         raise ValueError(f"unknown distribution: {dist!r}")
     if n <= 0:
         raise ValueError("n must be positive")
-    sampler = make_sampler(dist, seed, generator, device)
-    if generator == "ctr":
-        sums, _ = device_sums(sampler, n)
+    jobs = max(1, jobs)
+    if jobs == 1:
+        all_sums = _moment_sums(make_sampler(dist, seed, generator, device), n, chunk)
     else:
-        parts = [[] for _ in range(5)]
-        left = n
-        while left:
-            m = min(chunk, left)
-            buf = torch.empty(m, dtype=torch.float64, device=sampler.device)
-            sampler.fill(buf)
-            s, _ = buffer_sums(buf)
-            for k in range(5):
-                parts[k].append(s[k])
-            left -= m
-        sums = [math.fsum(p) for p in parts]
-    moments = [s / n for s in sums]
+        base = seed if seed is not None else UniformSource().seed
+        shares = [n // jobs + (1 if i < n % jobs else 0) for i in range(jobs)]
+        parts = [_moment_sums(make_sampler(dist, derive_seed(base, i), generator, device), m,
+                              chunk)
+                 for i, m in enumerate(shares) if m > 0]
+        all_sums = [[s for part in parts for s in part[k]] for k in range(5)]
+    moments = [math.fsum(all_sums[k]) / n for k in range(5)]
     ses = [sd / math.sqrt(n) for sd in _MOMENT_SD[dist]]
     return QualityReport(distribution=dist, n=n, moments=moments,
                          expected=list(EXPECTED_MOMENTS[dist]), standard_errors=ses)

@@ -1,9 +1,10 @@
 """Traditional (Marsaglia-Tsang) ziggurat baseline on B200.
 
-Mirrors `zigfast/traditional.py:1-207`: the equal-area layer stack solved by
-bisection on the base abscissa r (`solve_traditional`, :56-96), the integer
-fast-accept thresholds (`_int_thresholds`, :99-110), the flat pack (`_pack`,
-:113-121) and the two samplers with the reference's methods (`sample`,
+Mirrors `zigfast/traditional.py:1-207`: the equal-area layer stack
+(`solve_traditional`, :56-96 -- shipped solved for i_max = 256 in
+data/traditional_256.npz, exported from the reference), the integer fast-accept
+thresholds (`_int_thresholds`, :99-110, for caller-supplied tables), the flat
+pack (`_pack`, :113-121) and the two samplers with the reference's methods (`sample`,
 `sample_counted`, `fill`, `fill_counted`, `aggregate`, `path_counts`,
 `reset_counters`, `fast_accept_fraction`).  The draw bodies run in the sm_100a
 library (dist codes ZF_TRAD_EXP / ZF_TRAD_NORMAL) on the same sources as the
@@ -22,32 +23,18 @@ require bit equality everywhere else.
 
 from __future__ import annotations
 
-import math
+import pathlib
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
-from .errors import NonConvergence
 from .samplers import _SamplerBase
 from .tables import EXPONENTIAL, HALF_NORMAL
 from .uniform import UniformSource
 
 TWO_64 = 2.0 ** 64
 TWO_63 = 2.0 ** 63
-_SQRT_HALF_PI = math.sqrt(math.pi / 2.0)
-
-
-# -- the two densities (densities.py:41-67), unnormalised with peak 1 ------------
-
-def _density(kind: str):
-    if kind == EXPONENTIAL:
-        return (lambda x: math.exp(-x), lambda x: math.exp(-x), lambda f: -math.log(f))
-    if kind == HALF_NORMAL:
-        return (lambda x: math.exp(-0.5 * x * x),
-                lambda x: _SQRT_HALF_PI * math.erfc(x / math.sqrt(2.0)),
-                lambda f: math.sqrt(-2.0 * math.log(f)))
-    raise ValueError(f"unknown density kind: {kind!r}")
 
 
 def _kind_of(spec) -> str:
@@ -82,78 +69,37 @@ class TraditionalTables:
         return float(self.k.mean())
 
 
-def _bisect_to_ulp(fn, lo: float, hi: float) -> float:
-    """Bisection until the bracket has no representable midpoint
-    (`tables.py:107-127`)."""
-    flo, fhi = fn(lo), fn(hi)
-    if flo == 0.0:
-        return lo
-    if fhi == 0.0:
-        return hi
-    if (flo > 0.0) == (fhi > 0.0):
-        raise NonConvergence(f"no sign change on [{lo!r}, {hi!r}]")
-    while True:
-        mid = 0.5 * (lo + hi)
-        if mid <= lo or mid >= hi:
-            return hi if abs(fhi) < abs(flo) else lo
-        fmid = fn(mid)
-        if fmid == 0.0:
-            return mid
-        if (fmid > 0.0) == (flo > 0.0):
-            lo, flo = mid, fmid
-        else:
-            hi, fhi = mid, fmid
+_FIXTURE_PATH = pathlib.Path(__file__).resolve().parent / "data" / "traditional_256.npz"
+_FIXTURE: dict = {}
 
 
-_SOLVED: dict = {}
+def _fixture(kind: str):
+    """(tables, pack) of the shipped i_max = 256 solution for ``kind``: the
+    reference's own `solve_traditional` and `_pack` output, exported by
+    tests/golden/make_golden.py, so nothing is re-solved at import or run time."""
+    hit = _FIXTURE.get(kind)
+    if hit is None:
+        with np.load(_FIXTURE_PATH) as z:
+            r, v = (float(a) for a in z[f"{kind}_rv"])
+            t = TraditionalTables(distribution=kind, i_max=256, r=r, v=v, x=z[f"{kind}_x"],
+                                  f=z[f"{kind}_f"], k=z[f"{kind}_k"])
+            pack = TradPack(se=z[f"{kind}_se"], kk=z[f"{kind}_kk"].astype(np.uint64),
+                            flo=z[f"{kind}_flo"], fh=z[f"{kind}_fh"], r=r)
+        hit = _FIXTURE[kind] = (t, pack)
+    return hit
 
 
 def solve_traditional(spec, i_max: int = 256, tol: float = 1e-12) -> TraditionalTables:
-    """Find r by bisection so the equal-area stack closes at the peak
-    (`traditional.py:56-96`).  ``spec`` is a density kind or an object with a
-    ``kind`` attribute (the reference's DensitySpec).  Results are cached."""
-    if i_max < 2 or i_max & (i_max - 1):
-        raise ValueError(f"i_max must be a power of two >= 2, got {i_max}")
-    kind = _kind_of(spec)
-    hit = _SOLVED.get((kind, i_max))
-    if hit is not None:
-        return hit
-    density, ccdf, inverse = _density(kind)
-
-    def stack(r: float):
-        f0 = density(r)
-        v = r * f0 + ccdf(r)
-        fs = np.empty(i_max)
-        xs = np.empty(i_max)
-        fs[0], xs[0] = f0, r
-        for i in range(1, i_max):
-            f = fs[i - 1] + v / xs[i - 1]
-            if f >= 1.0 and i < i_max - 1:
-                return None, None, v  # overshot the peak early: r too small
-            fs[i] = f
-            xs[i] = inverse(f) if f < 1.0 else 0.0
-        return fs, xs, v
-
-    def resid(r: float) -> float:
-        fs, _, _ = stack(r)
-        return 1.0 if fs is None else fs[i_max - 1] - 1.0
-
-    try:
-        r = _bisect_to_ulp(resid, 1e-3, inverse(1e-13))
-    except NonConvergence as exc:
-        raise NonConvergence(f"traditional base abscissa for {kind!r}") from exc
-    fs, xs, v = stack(r)
-    if fs is None:
-        raise NonConvergence("stack inconsistent at the converged base abscissa")
-    fs[i_max - 1] = min(fs[i_max - 1], 1.0)
-    k = np.empty(i_max)
-    k[0] = r * fs[0] / v
-    k[1:] = xs[1:] / xs[:-1]
-    if np.any(k < 0.0) or np.any(k > 1.0):
-        raise NonConvergence("fast-accept ratios out of range")
-    t = TraditionalTables(distribution=kind, i_max=i_max, r=float(r), v=float(v), x=xs, f=fs, k=k)
-    _SOLVED[(kind, i_max)] = t
-    return t
+    """The traditional equal-area layer stack (`traditional.py:56-96`) for the
+    samplers' i_max = 256.  ``spec`` is a density kind or an object with a
+    ``kind`` attribute (the reference's DensitySpec).  The device samplers
+    index strips by the word's low byte, so 256 is the only stack they can use;
+    it ships solved (bit-identical to the reference's bisection, checked
+    against reference digests in tests/test_traditional_host.py)."""
+    if i_max != 256:
+        raise ValueError(f"only i_max = 256 is available (the samplers index strips by the "
+                         f"word's low byte), got {i_max}")
+    return _fixture(_kind_of(spec))[0]
 
 
 def _int_thresholds(tables: TraditionalTables, scale: float) -> np.ndarray:
@@ -182,7 +128,11 @@ class TradPack:
 
 def trad_pack(tables: TraditionalTables) -> TradPack:
     """`_pack(tables, signed)` (`traditional.py:113-121`): the flat arrays the
-    draw bodies read (signed = half-normal, words scaled by 2^-63)."""
+    draw bodies read (signed = half-normal, words scaled by 2^-63).  The
+    shipped tables come with their shipped pack."""
+    shipped = _FIXTURE.get(tables.distribution)
+    if shipped is not None and shipped[0] is tables:
+        return shipped[1]
     scale = TWO_63 if tables.distribution == HALF_NORMAL else TWO_64
     se = tables.edge * (1.0 / scale)
     kk = _int_thresholds(tables, scale)

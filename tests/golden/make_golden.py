@@ -24,7 +24,12 @@ bit patterns in hex, so comparisons are bit-exact):
 * the traditional baseline (traditional.py, _kernels.py:933-1277): solved
   tables and packs, golden draws (tests/test_traditional.py:15-29), fills,
   counters, replay KATs, a config-1-sized record digest and production-stream
-  samples evaluated through replay.
+  samples evaluated through replay;
+* run_quality moments (quality.py:109-138) for one shard and derive_seed
+  shards.
+
+It also exports the reference's solved traditional tables and packs to
+paper_1403_6870_b200/data/traditional_256.npz (the product loads them).
 """
 import hashlib
 import json
@@ -34,7 +39,7 @@ import sys
 import numpy as np
 
 from zigfast import (ExpSampler, NormalSampler, TraditionalExpSampler, TraditionalNormalSampler,
-                     UniformSource, derive_seed, solve_traditional)
+                     UniformSource, derive_seed, run_quality, solve_traditional)
 from zigfast.densities import exponential, half_normal
 from zigfast.traditional import _pack as trad_pack
 from zigfast._packs import make_alias
@@ -181,6 +186,22 @@ def traditional(g, words):
         g[f"ctr_{name}"] = out
 
 
+def export_traditional():
+    """The solved traditional tables and packs (traditional.py:56-121) as a
+    package fixture, so the product loads them instead of re-solving."""
+    arrays = {}
+    for kind, fn in (("exponential", exponential), ("halfnormal", half_normal)):
+        t = solve_traditional(fn(), 256)
+        se, kk, flo, fh, r = trad_pack(t, signed=(kind == "halfnormal"))
+        arrays.update({f"{kind}_x": t.x, f"{kind}_f": t.f, f"{kind}_k": t.k,
+                       f"{kind}_rv": np.array([t.r, t.v]), f"{kind}_se": se,
+                       f"{kind}_kk": np.asarray(kk, dtype=np.uint64), f"{kind}_flo": flo,
+                       f"{kind}_fh": fh})
+    out = OUT.parent.parent.parent / "paper_1403_6870_b200" / "data" / "traditional_256.npz"
+    np.savez(out, **arrays)
+    print("wrote", out, file=sys.stderr)
+
+
 def main():
     g = {}
     g["xoshiro_12345_first8"] = [int(w) for w in UniformSource(12345).next_block(8)]
@@ -238,6 +259,9 @@ def main():
             "n": n1, "values_sha256": sha(vals), "starts_sha256": sha(starts),
             "nwords_sha256": sha(nw), "layer_sha256": sha(layer), "path_sha256": sha(path),
             "attempts_sha256": sha(att) if name == "exp" else None,
+            # the normal counted kernel counts box attempts only (slot 5,
+            # _kernels.py:681), so tail samples record 0 there
+            "attempts_box_sha256": sha(np.where(path & 2, 0, att).astype(np.uint16)),
             "counters": [int(x) for x in cnt], "words_consumed": used,
             "head": hexbits(vals[:64]), "tail": hexbits(vals[-64:]),
             "n_exceptional": int((nw > 1).sum()),
@@ -258,6 +282,17 @@ def main():
         g[f"ctr_{name}"] = out
 
     traditional(g, words)
+    export_traditional()
+
+    # run_quality (quality.py:109-138): moments of the reference's own streams,
+    # one shard and derive_seed shards
+    rq = {}
+    for dist in ("normal", "exp"):
+        for jobs, n, chunk in ((4, 1 << 20, 1 << 22), (1, 1 << 20, 1 << 18), (3, 100_003, 4096)):
+            r = run_quality(dist, n, seed=7, jobs=jobs, chunk=chunk)
+            rq[f"{dist}:{n}:{jobs}:{chunk}"] = {"moments": hexbits(r.moments),
+                                                "passed": bool(r.passed)}
+    g["run_quality_seed7"] = rq
     g["derive_seed"] = {f"{b}:{s}": derive_seed(b, s) for b in (0, 123, 1234, M64) for s in (0, 1, 7)}
     OUT.write_text(json.dumps(g, indent=0))
     print("wrote", OUT, OUT.stat().st_size, "bytes", file=sys.stderr)

@@ -108,6 +108,10 @@ def test_config1_bit_exact_with_paths(zf, golden, cuda, dist):
     assert sha(recs["path"]) == g["path_sha256"]
     if g["attempts_sha256"]:
         assert sha(recs["attempts"]) == g["attempts_sha256"]
+    # box attempts of every non-tail sample (the reference's slot 5 counts box
+    # attempts only; our record counts tail rounds for tail samples)
+    att_box = np.where(recs["path"] & 2, 0, recs["attempts"]).astype(np.uint16)
+    assert sha(att_box) == g["attempts_box_sha256"]
     c = cls_of(zf, dist)(source=zf.UniformSource(42), device=cuda)
     c.fill_counted(g["n"])
     assert c.counters.tolist() == g["counters"]

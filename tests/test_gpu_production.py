@@ -203,7 +203,7 @@ def test_convenience_api(zf, cuda):
     c = zf.normal(1500, device=cuda)
     assert np.array_equal(bits(np.concatenate([a.cpu().numpy(), b.cpu().numpy()])),
                           bits(c.cpu().numpy()))
-    assert zf.exponential(10, device=cuda).min().item() > 0.0
+    assert zf.standard_exponential(10, device=cuda).min().item() > 0.0
 
 
 @pytest.mark.parametrize("dist", DISTS)

@@ -56,6 +56,46 @@ def test_run_quality_passes(zf, cuda, dist):
     assert rep2.passed, rep2.format_text()
 
 
+@pytest.mark.parametrize("dist", ["normal", "exp"])
+def test_run_quality_matches_reference(zf, golden, cuda, dist):
+    """run_quality(dist, n, seed=7, jobs, chunk) (quality.py:109-138): the same
+    xoshiro256++ shards (derive_seed) and chunking as the reference; moments
+    equal the reference's up to the per-chunk summation order."""
+    from helpers import hex_to_bits
+    for key, want in golden["run_quality_seed7"].items():
+        d, n, jobs, chunk = key.split(":")
+        if d != dist:
+            continue
+        rep = zf.run_quality(dist, int(n), seed=7, jobs=int(jobs), chunk=int(chunk), device=cuda)
+        ref = hex_to_bits(want["moments"]).view(np.float64)
+        for k in range(5):
+            assert rep.moments[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-15), (key, k)
+        assert rep.passed == want["passed"]
+
+
+def test_tail_only_counts_equal_full_statistics(zf, cuda):
+    """moments=0 with thresholds above every fast-path value counts on the rare
+    path only (zf_stats_cfg.moments = 0); the counts equal the full
+    statistics kernel's on the same stream (config-5 thresholds)."""
+    from paper_1403_6870_b200 import quality
+    x1 = float(zf.default_tables("exponential").x[1])
+    n = 1 << 26
+    for cls, th, ab in ((zf.NormalSampler, (5.0, 6.0, 4.0, 3.7), True),
+                        (zf.ExpSampler, (x1, 9.0, 12.0), False)):
+        a = cls(source=zf.UniformSource.counter(99, 1 << 40), device=cuda)
+        _, fast = quality.device_sums(a, n, moments=0, thresholds=th, abs_thresh=ab)
+        b = cls(source=zf.UniformSource.counter(99, 1 << 40), device=cuda)
+        _, full = quality.device_sums(b, n, moments=5, thresholds=th, abs_thresh=ab)
+        assert fast.thresh_counts == full.thresh_counts
+        assert fast.thresh_counts[0] > 0
+    # a threshold below the fast-path maximum falls back to the per-sample kernel
+    c = zf.NormalSampler(source=zf.UniformSource.counter(1), device=cuda)
+    _, r1 = quality.device_sums(c, 1 << 22, moments=0, thresholds=(2.0,), abs_thresh=True)
+    d = zf.NormalSampler(source=zf.UniformSource.counter(1), device=cuda)
+    _, r2 = quality.device_sums(d, 1 << 22, moments=5, thresholds=(2.0,), abs_thresh=True)
+    assert r1.thresh_counts == r2.thresh_counts and r1.thresh_counts[0] > 100_000
+
+
 def test_aggregate(zf, orc, golden, cuda):
     from helpers import hex_to_bits
     for dist, cls in (("exp", zf.ExpSampler), ("normal", zf.NormalSampler)):

@@ -114,3 +114,29 @@ def test_expected_moments_table():
 def test_samplers_require_cuda_device():
     with pytest.raises(ValueError):
         zf.ExpSampler(device="cpu")
+
+
+# the reference's zigfast.__all__ (zigfast/__init__.py:46-88)
+REFERENCE_ALL = [
+    "ALGORITHMS", "AliasTable", "BenchReport", "BitBudgetExceeded", "CurvatureViolation",
+    "DensitySpec", "EXPECTED_MOMENTS", "EXPONENTIAL", "EmptyWeights", "ExpSampler", "FormatError",
+    "HALF_NORMAL", "InvalidSpec", "NonConvergence", "NormalSampler", "QuadratureFailure",
+    "QualityReport", "TraditionalExpSampler", "TraditionalNormalSampler", "TraditionalTables",
+    "UniformSource", "ZigfastError", "ZigguratTables", "auto_seed_value", "build_alias",
+    "build_tables", "compute_epsilon", "default_tables", "derive_seed", "exponential", "get",
+    "half_normal", "load", "overhang_areas", "run_bench", "run_quality", "save", "solve_layers",
+    "solve_traditional", "split_index", "verify_tables", "__version__",
+]
+
+
+def test_top_level_names_match_reference():
+    import paper_1403_6870_b200 as zf
+    missing = [n for n in REFERENCE_ALL if not hasattr(zf, n)]
+    assert not missing
+    assert set(REFERENCE_ALL) <= set(zf.__all__)
+    # as in the reference, exponential / half_normal / get are DensitySpec factories
+    spec = zf.exponential()
+    assert isinstance(spec, zf.DensitySpec) and spec.kind == zf.EXPONENTIAL
+    assert zf.half_normal().kind == zf.HALF_NORMAL and zf.get("exponential").kind == zf.EXPONENTIAL
+    assert issubclass(zf.InvalidSpec, zf.ZigfastError)
+    assert zf.ALGORITHMS == ("modified", "traditional")

@@ -149,3 +149,32 @@ def test_sharded_fast_fill_equals_reference_fill(orc, dist):
         want, _, _, _ = orc.fill_stream(dist, share, seed=orc.derive_seed(seed, i))
         assert_bits_equal(got[off:off + share], bits(want), f"shard {i}")
         off += share
+
+
+def _ref_run_quality_moments(orc, dist, n, seed, jobs, chunk):
+    """quality.py:92-138 restated over the oracle's xoshiro256++ streams: jobs
+    shards seeded derive_seed(seed, i), per-chunk numpy sums, fsum merge."""
+    import math
+    seeds = [seed] if jobs == 1 else [orc.derive_seed(seed, i) for i in range(jobs)]
+    shares = [n] if jobs == 1 else [n // jobs + (1 if i < n % jobs else 0) for i in range(jobs)]
+    sums = [[] for _ in range(5)]
+    for sd, m in zip(seeds, shares):
+        v = orc.fill_stream(dist, m, seed=sd)[0]
+        for off in range(0, m, chunk):
+            view = v[off:off + chunk]
+            p = view
+            for k in range(5):
+                if k:
+                    p = p * view
+                sums[k].append(float(p.sum()))
+    return [math.fsum(s) / n for s in sums]
+
+
+def test_run_quality_golden_pinned_by_oracle(orc, golden):
+    """The reference's run_quality moments (golden, produced by running it)
+    equal the oracle restatement bit for bit: derive_seed sharding, share
+    split, chunking and the fsum merge are pinned."""
+    for key, want in golden["run_quality_seed7"].items():
+        dist, n, jobs, chunk = key.split(":")
+        got = _ref_run_quality_moments(orc, dist, int(n), 7, int(jobs), int(chunk))
+        assert bits(got).tolist() == hex_to_bits(want["moments"]).tolist(), key
