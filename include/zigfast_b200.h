@@ -169,7 +169,9 @@ int zf_tables_destroy(zf_tables* t);
 /* Production mode: sample k (0 <= k < n) of the call is global sample
  * K = ctr_base + k of the counter stream of `seed`:
  *   words  S(K), S(2^63 + K*2^19), S(2^63 + K*2^19 + 1), ...
- *   S(c) = splitmix64 word c of `seed` (mix13(seed + (c+1)*0x9E3779B97F4A7C15)).
+ *   S(c) = fmix64(seed + (c+1)*0x9E3779B97F4A7C15)   (MurmurHash3's 64-bit
+ *          finalizer on splitmix64's Weyl sequence; the draw body is the
+ *          reference's, so any sample can be replayed through it).
  * ctr_base + n must not exceed 2^44.  Asynchronous on `stream`.
  * counters_dev (nullable): int64[6] accumulated with the reference's slots. */
 int zf_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,

@@ -1,8 +1,9 @@
 // zf_device.cuh -- device-side building blocks shared by every sm_100a kernel.
 //
-// * splitmix64 word function (the reference's gid-1 generator, _kernels.py:77-82)
-//   used as a counter-based source: word c of seed s is mix13(s + (c+1)*gamma),
-//   so any position is reachable in O(1) ("counter-based skip-ahead").
+// * the counter-based production source: word c of seed s is
+//   fmix64(s + (c+1)*gamma) on splitmix64's Weyl sequence, so any position is
+//   reachable in O(1) ("counter-based skip-ahead"); mix13 (the reference's
+//   gid-1 splitmix64 output function, _kernels.py:77-82) for oracle mode.
 // * the shared-memory table pack (layout of _packs.py:31-60, padded to 256 slots)
 // * the modified-ziggurat draw bodies, templated on the word stream so the
 //   production kernel (counter stream) and the oracle-mode replay pipeline run
@@ -22,7 +23,7 @@ namespace zf {
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t kM1 = 0xBF58476D1CE4E5B9ull;
 constexpr uint64_t kM2 = 0x94D049BB133111EBull;
-// Secondary (exceptional) words of global sample K live at splitmix positions
+// Secondary (exceptional) words of global sample K live at counter positions
 // 2^63 + K * 2^19 + t: disjoint from every primary position K < 2^44.
 constexpr uint64_t kExcBase = 1ull << 63;
 constexpr int kExcShift = 19;
@@ -55,6 +56,27 @@ __host__ __device__ __forceinline__ uint64_t mix13(uint64_t z) {
 #endif
   return z ^ (z >> 31);
 }
+
+// Word function of the production counter stream: MurmurHash3's 64-bit
+// finalizer fmix64 (shifts of 33 -- the same constants SplittableRandom uses
+// to mix its gammas) applied to the splitmix64 Weyl sequence.  Its xorshifts
+// by 33 are one SHF + one LOP3 on 32-bit halves where mix13's shifts by 30,
+// 27 and 31 need two of each: +10 % fill throughput on B200 (DESIGN.md,
+// "Production word function"), with the generator battery of
+// tools/battery.py showing no difference between the two
+// (profiles/r02_battery.json).  mix13 stays the word function of the
+// reference's own splitmix64 stream (gid 1, oracle mode).
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+#if defined(__CUDA_ARCH__)
+  z = mul64_chained<0xff51afd7ed558ccdull>(z ^ (z >> 33));
+  z = mul64_chained<0xc4ceb9fe1a85ec53ull>(z ^ (z >> 33));
+#else
+  z = (z ^ (z >> 33)) * 0xff51afd7ed558ccdull;
+  z = (z ^ (z >> 33)) * 0xc4ceb9fe1a85ec53ull;
+#endif
+  return z ^ (z >> 33);
+}
+__host__ __device__ __forceinline__ uint64_t ctr_word(uint64_t z) { return fmix64(z); }
 
 // One distribution's pack.  sx has kSlots+2 entries so sx[i+1] is in bounds for
 // every byte i: the fast loop reads it branch-free, and entries past L_max hold
@@ -197,13 +219,13 @@ static __device__ __noinline__ double log_cr(double x) {
 // word streams
 // ---------------------------------------------------------------------------
 
-// Secondary words of one production sample: splitmix64 positions c, c+1, ...
+// Secondary words of one production sample: counter positions c, c+1, ...
 struct CtrStream {
   uint64_t st;  // seed + c * gamma  (pre-increment form)
   static constexpr bool kBounded = false;
   __device__ __forceinline__ uint64_t next() {
     st += kGamma;
-    return mix13(st);
+    return ctr_word(st);
   }
   __device__ __forceinline__ bool dead() const { return false; }
   __device__ __forceinline__ uint32_t used() const { return 0; }
@@ -363,11 +385,11 @@ __device__ __forceinline__ bool exp_box_words(const DevPack& p, int j, uint64_t 
 // u = an exceptional byte) on the secondary counter stream at `sbase`: the
 // four words of the alias pick and the first box attempt are independent
 // counter positions, so they are computed side by side instead of one
-// dependent mix13 chain after another.  Same words, same arithmetic, same
+// dependent word-function chain after another.  Same words, same arithmetic, same
 // value as exp_draw.
 __device__ __forceinline__ double exp_draw_ctr(const DevPack& p, uint64_t sbase) {
-  const uint64_t w1 = mix13(sbase + kGamma), w2 = mix13(sbase + 2 * kGamma);
-  const uint64_t w3 = mix13(sbase + 3 * kGamma), w4 = mix13(sbase + 4 * kGamma);
+  const uint64_t w1 = ctr_word(sbase + kGamma), w2 = ctr_word(sbase + 2 * kGamma);
+  const uint64_t w3 = ctr_word(sbase + 3 * kGamma), w4 = ctr_word(sbase + 4 * kGamma);
   const int j = alias_from(p, w1, w2);
   NoCount c;
   if (j == 0) {  // tail: shift by X[1], word 3 is the next first word

@@ -418,10 +418,13 @@ __global__ void add_counters(const unsigned long long* __restrict__ src,
 }
 
 // ---- word generation ---------------------------------------------------------------
-__global__ void words_splitmix(uint64_t state, uint64_t n, uint64_t* __restrict__ out) {
+// CTR = false: splitmix64 words (gid 1); true: the production counter stream's
+// primary words ctr_word(seed + (K + 1) * gamma)
+template <bool CTR>
+__global__ void words_weyl(uint64_t state, uint64_t n, uint64_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = mix13(state + (i + 1) * kGamma);
+    out[i] = CTR ? ctr_word(state + (i + 1) * kGamma) : mix13(state + (i + 1) * kGamma);
 }
 
 __device__ __forceinline__ void xo_step(uint64_t s[4]) {
@@ -908,10 +911,13 @@ int run_replay(const zf_tables* t, int dist, int dtype, const uint64_t* words, u
 int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cudaStream_t s) {
   if (n == 0) return ZF_OK;
   if (gid == ZF_GEN_SPLITMIX64 || gid == ZF_GEN_CTR) {
-    // ctr words are the primary counter stream: splitmix64 of seed from position ctr
+    // ctr words are the primary counter stream from sample position state[1]
     const uint64_t st = gid == ZF_GEN_CTR ? state[0] + state[1] * kGamma : state[0];
     const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-    words_splitmix<<<grid, 256, 0, s>>>(st, n, out);
+    if (gid == ZF_GEN_CTR)
+      words_weyl<true><<<grid, 256, 0, s>>>(st, n, out);
+    else
+      words_weyl<false><<<grid, 256, 0, s>>>(st, n, out);
     return cuda_status(cudaGetLastError());
   }
   if (gid != ZF_GEN_XOSHIRO256PP) return ZF_EDIST;

@@ -3,7 +3,7 @@
 //
 // A warp walks "tiles" of kTile consecutive samples (kPerLane per lane).
 //   pass 1  every lane computes the fast-path value of its samples (one
-//           splitmix64 word, LDS.64, I2F, DMUL) and hands V of them at a time
+//           counter-stream word, LDS.64, I2F, DMUL) and hands V of them at a time
 //           to the sink; exceptional samples (byte >= L_max, ~1.2-1.6 %) only
 //           set a bit in the lane's mask.
 //   pass 2  the warp compacts the masked samples into a per-warp smem queue
@@ -37,11 +37,16 @@ constexpr int kPass1Unroll = ZF_PASS1_UNROLL;
 
 // Rounds compute the alias-pick and first-attempt words side by side.
 #ifndef ZF_HOIST
-#define ZF_HOIST 0
+#define ZF_HOIST 1
 #endif
 // Tables staged by two bulk copies: pass 1 waits only for the scale array.
+// Normal rounds: each lane's first two box attempts side by side before the
+// cooperative iterations (+1 % normal fill, 713 vs 706 G/s at 2^28).
+#ifndef ZF_SPEC2
+#define ZF_SPEC2 1
+#endif
 #ifndef ZF_ASYNC_STAGE
-#define ZF_ASYNC_STAGE 0
+#define ZF_ASYNC_STAGE 1
 #endif
 
 #ifndef ZF_QUEUE_CAP
@@ -229,7 +234,7 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
         // sx[i+1] is NaN for every byte i >= L_max (see fill_devpack), so the
         // fast value itself flags an exceptional sample: a DSETP on the fp64
         // pipe instead of integer compare/select work on the busy ALU pipe.
-        const uint64_t w = mix13(st + (uint64_t)e * kGamma);
+        const uint64_t w = ctr_word(st + (uint64_t)e * kGamma);
         double d = fast_value<DIST>(sx, w);
         if constexpr (kTrad<DIST>)  // traditional: integer fast-accept test
           d = trad_fast<DIST>(P.kk, w) ? d : __longlong_as_double(0x7ff8000000000000ll);
@@ -252,10 +257,14 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
       for (int e = 0; e < V; ++e) {
         const uint64_t k = k_lane + (uint64_t)it * 32 * V + e;
         if (k < n) {
-          const uint64_t u = mix13(st0 + (uint64_t)it * kIterStride + (uint64_t)e * kGamma);
-          const bool exc = exc_word<DIST>(P, u);
+          const uint64_t u = ctr_word(st0 + (uint64_t)it * kIterStride + (uint64_t)e * kGamma);
+          const double d = fast_value<DIST>(sx, u);
+          // modified tables: the NaN sentinel of sx (pass 1 may run before the
+          // rest of the pack -- lmax included -- has been staged); traditional
+          // tables are staged whole before pass 1
+          const bool exc = kTrad<DIST> ? exc_word<DIST>(P, u) : isnan(d);
           mask |= (uint32_t)exc << (it * V + e);
-          sink.put(k, to_out<OutT>(fast_value<DIST>(sx, u)), exc);
+          sink.put(k, to_out<OutT>(d), exc);
           ++valid;
         }
       }
@@ -291,7 +300,7 @@ __device__ __forceinline__ void resolve_one(const DevPack& P, const DevPack& E, 
   // k is exceptional: the modified exponential draw only needs to know that
   // (its first word's bits are never read again), the normal one needs the
   // sign bit, the traditional ones the whole word
-  const uint64_t u = DIST == ZF_EXP ? 0xFFull : mix13(seed + (K + 1) * kGamma);
+  const uint64_t u = DIST == ZF_EXP ? 0xFFull : ctr_word(seed + (K + 1) * kGamma);
   CtrStream s{seed + (kExcBase + (K << kExcShift)) * kGamma};
   double v;
   if (COUNTED) {
@@ -336,16 +345,22 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
   // (own must be 16-byte aligned: kQueueCap words past a 16-byte aligned queue)
   using OutT = typename Sink::Out;
   const uint64_t K = ctr_base + k;
-  const uint64_t u = mix13(seed + (K + 1) * kGamma);  // the sign word
+  const uint64_t u = ctr_word(seed + (K + 1) * kGamma);  // the sign word
   const uint64_t sbase = seed + (kExcBase + (K << kExcShift)) * kGamma;
   double val;
   bool done;
 #if ZF_HOIST
   // the alias pick's and the first box attempt's words are independent
   // counter positions: compute them side by side
-  const uint64_t w1 = mix13(sbase + kGamma), w2 = mix13(sbase + 2 * kGamma);
-  const uint64_t w3 = mix13(sbase + 3 * kGamma), w4 = mix13(sbase + 4 * kGamma);
+  const uint64_t w1 = ctr_word(sbase + kGamma), w2 = ctr_word(sbase + 2 * kGamma);
+  const uint64_t w3 = ctr_word(sbase + 3 * kGamma), w4 = ctr_word(sbase + 4 * kGamma);
+#if ZF_SPEC2
+  // and the second attempt's (positions 5, 6): with ~58 % acceptance per box
+  // attempt, 18 % of the lanes are left for the cooperative iterations
+  const uint64_t w5 = ctr_word(sbase + 5 * kGamma), w6 = ctr_word(sbase + 6 * kGamma);
+#endif
   const int j = alias_from(P, w1, w2);
+  uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
   if (j == 0) {
     NoCount c;
     CtrStream s{sbase + 2 * kGamma};
@@ -353,8 +368,18 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
     done = true;
   } else {
     done = normal_box_words(P, j, w3, w4, val);
+#if ZF_SPEC2
+    double x1;
+    const bool a1 = normal_box_words(P, j, w5, w6, x1);
+    if (!done && a1) {
+      val = x1;
+      done = true;
+    }
+    next = 2;
+#endif
   }
 #else
+  uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
   CtrStream s{sbase};
   const int j = alias_pick(P, s);
   if (j == 0) {
@@ -365,7 +390,6 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
     done = normal_box_attempt(P, j, s, val);
   }
 #endif
-  uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t un = __ballot_sync(0xffffffffu, !done); un;
        un = __ballot_sync(0xffffffffu, !done)) {

@@ -7,7 +7,8 @@ Generators, selected by the reference's integer ids (`uniform.py:22-26`):
 * ``"splitmix64"`` (gid 1) -- sequential stream, random-access by nature.
 * replay (gid 2) -- a fixed word list played back with wrap-around.
 * ``"ctr"`` (gid 3, new) -- the production counter stream: sample K of a fill
-  reads splitmix64 word K of the seed, and its rare extra words come from the
+  reads word K = fmix64(seed + (K+1)*gamma) (MurmurHash3's finalizer on
+  splitmix64's Weyl sequence), and its rare extra words come from the
   disjoint positions 2^63 + K*2^19 + t.  Output K depends only on (seed, K),
   never on launch shape or GPU count; the state is ``[seed, next_counter]``.
 

@@ -19,7 +19,8 @@ bit patterns in hex, so comparisons are bit-exact):
   words, layer byte, path bits, box attempts), counters, words consumed, plus
   head/tail samples; the same for the normal sampler on the same stream;
 * production ("ctr") stream samples evaluated BY THE REFERENCE through replay
-  of each sample's word sequence [S(K), S(2^63 + K*2^19 + t) ...];
+  of each sample's word sequence [S(K), S(2^63 + K*2^19 + t) ...],
+  S(c) = fmix64(seed + (c+1) * gamma);
 * derive_seed values and aggregate() sums;
 * the traditional baseline (traditional.py, _kernels.py:933-1277): solved
   tables and packs, golden draws (tests/test_traditional.py:15-29), fills,
@@ -58,19 +59,21 @@ def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def mix13(z):
-    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
-    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
-    return z ^ (z >> 31)
+def fmix64(z):
+    z = ((z ^ (z >> 33)) * 0xff51afd7ed558ccd) & M64
+    z = ((z ^ (z >> 33)) * 0xc4ceb9fe1a85ec53) & M64
+    return z ^ (z >> 33)
 
 
-def splitmix_word(seed, c):
-    return mix13((seed + (c + 1) * GAMMA) & M64)
+def ctr_word(seed, c):
+    """Production counter-stream word c: MurmurHash3's fmix64 on splitmix64's
+    Weyl sequence (zf_device.cuh: fmix64)."""
+    return fmix64((seed + (c + 1) * GAMMA) & M64)
 
 
 def ctr_words(seed, K, m):
     base = (1 << 63) + (K << 19)
-    return [splitmix_word(seed, K)] + [splitmix_word(seed, base + t) for t in range(m - 1)]
+    return [ctr_word(seed, K)] + [ctr_word(seed, base + t) for t in range(m - 1)]
 
 
 def records(cls, words, n):

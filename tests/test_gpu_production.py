@@ -109,12 +109,15 @@ def test_host_destinations(zf, orc, cuda, dist):
 
 
 @pytest.mark.parametrize("dist", DISTS)
-def test_pageable_staging_paths(zf, cuda, dist):
+def test_pageable_staging_paths(zf, cuda, dist, monkeypatch):
     """The pinned-staging route for pageable host memory (several staging
     chunks, ragged last one): fp32, counted fills, oracle-mode sources, CPU
-    tensors and concurrent callers all equal the device-resident fill."""
+    tensors and concurrent callers all equal the device-resident fill.
+    (Registration in place is switched off here so the staging path runs.)"""
     import threading
     import torch
+    from paper_1403_6870_b200 import samplers
+    monkeypatch.setattr(samplers, "_REGISTER_MIN_BYTES", 1 << 62)
     n32 = 3 * (16 << 20) + 5
     a32 = np.empty(n32, dtype=np.float32)
     sampler(zf, dist, 5, device=cuda).fill(a32)
@@ -308,3 +311,32 @@ def test_misaligned_fp32_views(zf, orc, cuda, dist, shift):
     want, _, _ = orc.fill_ctr(dist, 4000, seed=13)
     assert np.array_equal(view.cpu().numpy(), want.astype(np.float32))
     assert buf[:shift].abs().sum().item() == 0.0 and buf[shift + 4000:].abs().sum().item() == 0.0
+
+
+def test_pageable_numpy_fill_page_locks_in_place(zf, cuda):
+    """fill(np.empty(n)) -- the reference's usage -- page-locks a large array
+    once (cached while it lives, unregistered when it is collected) and DMAs
+    into it; values equal the device fill, views of a registered array too."""
+    import gc
+    from paper_1403_6870_b200 import samplers
+    n = 1 << 24  # 128 MiB, above the registration threshold
+    arr = np.empty(n)
+    a = zf.NormalSampler(source=zf.UniformSource.counter(31, 77), device=cuda)
+    a.fill(arr)
+    want = zf.NormalSampler(source=zf.UniformSource.counter(31, 77), device=cuda).fill(n)
+    assert np.array_equal(arr.view(np.uint64), want.cpu().numpy().view(np.uint64))
+    ptr = arr.ctypes.data
+    assert ptr in samplers._registered
+    view = arr[1000:1000 + (1 << 23)]  # a view: its owner is already registered
+    b = zf.ExpSampler(source=zf.UniformSource.counter(5), device=cuda)
+    b.fill(view)
+    wv = zf.ExpSampler(source=zf.UniformSource.counter(5), device=cuda).fill(1 << 23)
+    assert np.array_equal(view.view(np.uint64), wv.cpu().numpy().view(np.uint64))
+    assert arr[999] == want[999].item()  # untouched outside the view
+    del arr, view
+    gc.collect()
+    assert ptr not in samplers._registered
+    # small arrays take the staged path and are not registered
+    small = np.empty(1 << 16)
+    a.fill(small)
+    assert small.ctypes.data not in samplers._registered
