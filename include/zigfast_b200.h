@@ -30,6 +30,7 @@
  *   zf_fill_stats      bench_exp / bench_normal + quality sums          _kernels.py:306-393, quality.py:92-106
  *   zf_stats           quality._moment_sums on a device buffer         quality.py:92-106
  *   zf_fill_batch      many (sampler, fill(8192)) requests, one launch  exponential.py:45-50
+ *   zf_batch_*         the same with the request table resident on the device
  *   zf_format_g17      gen --format text: f"{v:.17g}\n" per value       cli.py:100-120
  */
 #ifndef ZIGFAST_B200_H
@@ -146,6 +147,7 @@ typedef struct zf_stats_cfg {
 } zf_stats_cfg;
 
 typedef struct zf_tables zf_tables; /* opaque, immutable, thread-safe */
+typedef struct zf_batch zf_batch;   /* opaque: a request table resident on a device */
 
 int zf_abi_version(void);
 const char* zf_strerror(int status);
@@ -243,6 +245,17 @@ uint64_t zf_format_scratch_words(uint64_t n);
  * back.  Thread-safe per handle.  Asynchronous otherwise. */
 int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                   void* out_dev, void* stream);
+
+/* The same batch with its request table uploaded once to the handle's device
+ * (synchronously, by zf_batch_create): every zf_batch_fill is then a single
+ * launch with no host-side work -- a caller serving the same request layout
+ * repeatedly (BatchPlan.fill, batch.py) pays the table build and upload once.
+ * The batch keeps a pointer to `t`, which must outlive it. */
+int zf_batch_create(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
+                    zf_batch** out);
+int zf_batch_fill(const zf_batch* b, void* out_dev, void* stream);
+int zf_batch_destroy(zf_batch* b);
+const zf_tables* zf_batch_tables(const zf_batch* b);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,8 @@ EXPORTS = (
     "zf_fill_stats", "zf_stats", "zf_stats_blocks", "zf_fill_replay", "zf_fill_gid", "zf_words",
     "zf_xoshiro_jump", "zf_xoshiro_pow2_poly", "zf_fill_batch", "zf_trad_tables_create",
     "zf_format_g17", "zf_format_scratch_words", "zf_tables_create_default",
-    "zf_trad_tables_create_default",
+    "zf_trad_tables_create_default", "zf_batch_create", "zf_batch_fill", "zf_batch_destroy",
+    "zf_batch_tables",
 )
 EXP, NORMAL, TRAD_EXP, TRAD_NORMAL = 0, 1, 2, 3
 
@@ -103,6 +104,10 @@ def lib():
                 "zf_format_scratch_words": (u64, [u64]),
                 "zf_tables_create_default": (i32, [i32, C.POINTER(vp)]),
                 "zf_trad_tables_create_default": (i32, [i32, C.POINTER(vp)]),
+                "zf_batch_create": (i32, [vp, C.POINTER(Request), i32, i32, C.POINTER(vp)]),
+                "zf_batch_fill": (i32, [vp, vp, vp]),
+                "zf_batch_destroy": (i32, [vp]),
+                "zf_batch_tables": (vp, [vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

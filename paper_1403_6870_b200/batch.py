@@ -3,10 +3,12 @@
 The reference serves a request with a new sampler + `fill(8192)`
 (`exponential.py:26-50`), paying the alias build and a kernel dispatch every
 time.  Here a :class:`BatchPlan` lays many requests out back to back once
-(numpy, no per-request Python objects) and `fill` runs them all in ONE launch
-of `zf_fill_batch`; request r draws samples ctr_base..ctr_base+n-1 of the
-counter stream of its own seed, so each request's values equal a standalone
-`UniformSource.counter(seed, ctr_base)` fill.
+(numpy, no per-request Python objects) and `fill` runs them all in ONE launch;
+request r draws samples ctr_base..ctr_base+n-1 of the counter stream of its
+own seed, so each request's values equal a standalone
+`UniformSource.counter(seed, ctr_base)` fill.  The plan's request table is
+uploaded to a device once (`zf_batch_create`) and stays there, so every
+`fill` is a single launch with no host-side table work (`zf_batch_fill`).
 """
 
 from __future__ import annotations
@@ -50,6 +52,26 @@ class BatchPlan:
         self.offsets = offs.astype(np.int64)
         self.total = int(padded.sum()) if m else 0
         self.esz = esz
+        self._resident = {}  # device index -> (tables handle, zf_batch handle)
+
+    def _batch(self, dev):
+        hit = self._resident.get(dev.index)
+        if hit is None:
+            tabs = _lib.device_tables(default_tables(EXPONENTIAL), default_tables(HALF_NORMAL),
+                                      dev.index)
+            h = C.c_void_p()
+            _lib.check(_lib.lib().zf_batch_create(
+                tabs.handle, self.req.ctypes.data_as(C.POINTER(_lib.Request)), self.req.size,
+                _lib.F64 if self.esz == 8 else _lib.F32, C.byref(h)))
+            hit = self._resident[dev.index] = (tabs, h)
+        return hit[1]
+
+    def __del__(self):
+        try:
+            for _, h in getattr(self, "_resident", {}).values():
+                _lib.lib().zf_batch_destroy(h)
+        except Exception:  # interpreter shutdown
+            pass
 
     def fill(self, out=None, device=None):
         """One launch for every request; returns the output tensor."""
@@ -61,13 +83,9 @@ class BatchPlan:
             out = torch.empty(self.total, dtype=self.tdtype, device=dev)
         elif out.numel() < self.total or out.dtype != self.tdtype or not out.is_contiguous():
             raise ValueError("output tensor too small, wrong dtype or not contiguous")
-        tabs = _lib.device_tables(default_tables(EXPONENTIAL), default_tables(HALF_NORMAL),
-                                  dev.index)
         with torch.cuda.device(dev):
-            _lib.check(_lib.lib().zf_fill_batch(
-                tabs.handle, self.req.ctypes.data_as(C.POINTER(_lib.Request)), self.req.size,
-                _lib.F64 if self.esz == 8 else _lib.F32, out.data_ptr(),
-                _lib.stream_handle(dev)))
+            _lib.check(_lib.lib().zf_batch_fill(self._batch(dev), out.data_ptr(),
+                                                _lib.stream_handle(dev)))
         return out
 
     def view(self, out, i: int):
@@ -78,9 +96,20 @@ class BatchPlan:
 
 def fill_batch(requests, dtype="float64", device=None):
     """Convenience wrapper: ``requests`` = iterable of (dist, n, seed[, ctr_base]).
-    Returns (output tensor, offsets)."""
+    One-shot (`zf_fill_batch`: the request table goes through a pinned
+    staging ring, nothing stays resident).  Returns (output tensor, offsets)."""
+    import torch
     reqs = list(requests)
     plan = BatchPlan([r[0] for r in reqs], [int(r[1]) for r in reqs],
                      [int(r[2]) & ((1 << 64) - 1) for r in reqs],
                      [int(r[3]) if len(r) > 3 else 0 for r in reqs], dtype=dtype)
-    return plan.fill(device=device), [int(o) for o in plan.offsets]
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(plan.total, dtype=plan.tdtype, device=dev)
+    tabs = _lib.device_tables(default_tables(EXPONENTIAL), default_tables(HALF_NORMAL), dev.index)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().zf_fill_batch(
+            tabs.handle, plan.req.ctypes.data_as(C.POINTER(_lib.Request)), plan.req.size,
+            _lib.F64 if plan.esz == 8 else _lib.F32, out.data_ptr(), _lib.stream_handle(dev)))
+    return out, [int(o) for o in plan.offsets]

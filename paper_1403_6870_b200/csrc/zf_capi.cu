@@ -340,4 +340,24 @@ int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtyp
   return launch_fill_batch(t, reqs, nreq, dtype, out_dev, as_stream(stream));
 }
 
+int zf_batch_create(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
+                    zf_batch** out) {
+  if (!t || !out) return ZF_EINVAL;
+  *out = nullptr;
+  ZF_ON_DEVICE(t);
+  return batch_create(t, reqs, nreq, dtype, out);
+}
+
+int zf_batch_fill(const zf_batch* b, void* out_dev, void* stream) {
+  if (!b || !out_dev) return ZF_EINVAL;
+  ZF_ON_DEVICE(zf_batch_tables(b));
+  return batch_fill(b, out_dev, as_stream(stream));
+}
+
+int zf_batch_destroy(zf_batch* b) {
+  if (!b) return ZF_OK;
+  ZF_ON_DEVICE(zf_batch_tables(b));
+  return batch_destroy(b);
+}
+
 }  // extern "C"

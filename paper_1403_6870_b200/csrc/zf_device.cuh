@@ -281,11 +281,14 @@ struct Count {
 
 // The rejection test `y < exp(arg)` (_kernels.py:178, :492) with the decision
 // of the full double-precision exp, at a fraction of its cost: an fp32
-// MUFU-based estimate e = __expf(arg) has relative error below 2e-6 for
-// |arg| <= 20 (10 fp32 ulp of __expf plus the rounding of arg), so whenever y
-// lies outside e * (1 -+ 1e-5) the comparison with ANY exp within 1 ulp of
-// the true value (CUDA's exp, glibc's in the reference) is already decided.
-// Only the ~1e-5 of tests inside the band evaluate the double exp.
+// MUFU-based estimate e = __expf(arg) is within 2 + floor(1.16 |arg|) fp32
+// ulp of exp(float(arg)) (the CUDA guide's bound for __expf: 25 ulp = 3.0e-6
+// relative at |arg| = 20), and rounding arg to fp32 moves exp by at most
+// |arg| 2^-24 = 1.2e-6 relative, so for |arg| <= 20 e is within 4.2e-6 of
+// the true value.  Whenever y lies outside e * (1 -+ 1e-5) the comparison
+// with ANY exp within 1 ulp of the true value (CUDA's exp, glibc's in the
+// reference) is already decided; only the ~1e-5 of tests inside the band
+// evaluate the double exp.
 __device__ __forceinline__ bool less_than_exp(double y, double arg) {
   constexpr double kTol = 1e-5;
   if (fabs(arg) <= 20.0) {

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <vector>
 
 #include "zf_internal.h"
@@ -250,34 +251,74 @@ static int launch_batch_typed(const zf_tables* t, const DevRequest* dreq,
   return cuda_status(cudaGetLastError());
 }
 
-int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
-                      cudaStream_t s) {
-  if (nreq <= 0) return nreq == 0 ? ZF_OK : ZF_EINVAL;
-  if (t->kind != kKindModified) return ZF_ETABLE;
+// A batch's device image: the request table, then the chunk -> request map.
+// Chunk ids: every exponential request's chunks first, then the normal ones --
+// a warp strides through the ids, so it switches distribution at most once
+// instead of at every chunk (requests usually alternate; with alternating
+// chunks a third of the stalls were instruction fetches).
+struct BatchShape {
+  uint64_t per_dist[2] = {0, 0};
+  uint64_t chunks = 0;
+  bool vec = true;  // every request keeps the output's 16-byte alignment
+  size_t bytes(int nreq) const {
+    return sizeof(DevRequest) * (size_t)nreq + sizeof(uint32_t) * chunks;
+  }
+};
+
+static uint64_t chunks_of(uint64_t n) {
+  return ((n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;
+}
+
+static int batch_shape(const zf_request* reqs, int nreq, int dtype, BatchShape* sh) {
   if (dtype != ZF_F64 && dtype != ZF_F32) return ZF_EDIST;
   const size_t esz = dtype == ZF_F64 ? 8 : 4;
-  // every request must keep 16-byte alignment for the vector path
-  bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  std::vector<DevRequest> h((size_t)nreq);
-  // chunk ids: every exponential request's chunks first, then the normal ones.
-  // A warp strides through the ids, so it switches distribution at most once
-  // instead of at every chunk (requests usually alternate): with alternating
-  // chunks a third of the stalls were instruction fetches
-  uint64_t per_dist[2] = {0, 0};
   for (int i = 0; i < nreq; ++i) {
     const zf_request& r = reqs[i];
     if (r.dist != ZF_EXP && r.dist != ZF_NORMAL) return ZF_EDIST;
     if (r.ctr_base > kMaxCtr || r.n > kMaxCtr - r.ctr_base) return ZF_ERANGE;
-    if ((r.out_offset * esz) & 15) vec = false;
-    per_dist[r.dist] += ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;
+    if ((r.out_offset * esz) & 15) sh->vec = false;
+    sh->per_dist[r.dist] += chunks_of(r.n);
   }
-  const uint64_t chunks = per_dist[0] + per_dist[1];
-  if (chunks == 0) return ZF_OK;
-  if (chunks > 0xFFFFFFFFull) return ZF_ERANGE;
-  // one upload: the request table, then the chunk -> request map, staged in
-  // the handle's pinned ring slot
-  const size_t req_bytes = sizeof(DevRequest) * (size_t)nreq;
-  const size_t bytes = req_bytes + sizeof(uint32_t) * chunks;
+  sh->chunks = sh->per_dist[0] + sh->per_dist[1];
+  return sh->chunks > 0xFFFFFFFFull ? ZF_ERANGE : ZF_OK;
+}
+
+static void batch_write(const zf_request* reqs, int nreq, const BatchShape& sh,
+                        unsigned char* dst) {
+  DevRequest* h = reinterpret_cast<DevRequest*>(dst);
+  uint32_t* cmap = reinterpret_cast<uint32_t*>(dst + sizeof(DevRequest) * (size_t)nreq);
+  uint64_t next[2] = {0, sh.per_dist[0]};
+  for (int i = 0; i < nreq; ++i) {
+    const zf_request& r = reqs[i];
+    const uint64_t nc = chunks_of(r.n);
+    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, next[r.dist], r.dist, 0};
+    for (uint64_t c = 0; c < nc; ++c) cmap[next[r.dist] + c] = (uint32_t)i;
+    next[r.dist] += nc;
+  }
+}
+
+static int launch_batch_image(const zf_tables* t, const unsigned char* dev_image, int nreq,
+                              const BatchShape& sh, int dtype, void* out, cudaStream_t s) {
+  const DevRequest* dr = reinterpret_cast<const DevRequest*>(dev_image);
+  const uint32_t* dm =
+      reinterpret_cast<const uint32_t*>(dev_image + sizeof(DevRequest) * (size_t)nreq);
+  const bool vec = sh.vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (dtype == ZF_F64)
+    return vec ? launch_batch_typed<double, true>(t, dr, dm, sh.chunks, (double*)out, s)
+               : launch_batch_typed<double, false>(t, dr, dm, sh.chunks, (double*)out, s);
+  return vec ? launch_batch_typed<float, true>(t, dr, dm, sh.chunks, (float*)out, s)
+             : launch_batch_typed<float, false>(t, dr, dm, sh.chunks, (float*)out, s);
+}
+
+// One-shot batch: the image goes through the handle's pinned staging ring.
+int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
+                      cudaStream_t s) {
+  if (nreq <= 0) return nreq == 0 ? ZF_OK : ZF_EINVAL;
+  if (t->kind != kKindModified) return ZF_ETABLE;
+  BatchShape sh;
+  ZF_TRY_STATUS(batch_shape(reqs, nreq, dtype, &sh));
+  if (sh.chunks == 0) return ZF_OK;
+  const size_t bytes = sh.bytes(nreq);
   std::lock_guard<std::mutex> lock(t->stage.mu);
   BatchStage& sl = t->stage.slot[t->stage.next];
   t->stage.next = (t->stage.next + 1) % kStageSlots;
@@ -298,29 +339,59 @@ int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int 
     if (e == cudaSuccess && !sl.done) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
     ZF_TRY(e);
   }
-  uint32_t* cmap = reinterpret_cast<uint32_t*>(sl.host + req_bytes);
-  uint64_t next[2] = {0, per_dist[0]};
-  for (int i = 0; i < nreq; ++i) {
-    const zf_request& r = reqs[i];
-    const uint64_t nc = ((r.n + kTile - 1) / kTile + kBatchChunk - 1) / kBatchChunk;
-    h[i] = DevRequest{r.seed, r.ctr_base, r.n, r.out_offset, next[r.dist], r.dist, 0};
-    for (uint64_t c = 0; c < nc; ++c) cmap[next[r.dist] + c] = (uint32_t)i;
-    next[r.dist] += nc;
-  }
-  std::memcpy(sl.host, h.data(), req_bytes);
+  batch_write(reqs, nreq, sh, sl.host);
   ZF_TRY(cudaMemcpyAsync(sl.dev, sl.host, bytes, cudaMemcpyHostToDevice, s));
-  const DevRequest* dr = reinterpret_cast<const DevRequest*>(sl.dev);
-  const uint32_t* dm = reinterpret_cast<const uint32_t*>(sl.dev + req_bytes);
-  int status;
-  if (dtype == ZF_F64)
-    status = vec ? launch_batch_typed<double, true>(t, dr, dm, chunks, (double*)out, s)
-                 : launch_batch_typed<double, false>(t, dr, dm, chunks, (double*)out, s);
-  else
-    status = vec ? launch_batch_typed<float, true>(t, dr, dm, chunks, (float*)out, s)
-                 : launch_batch_typed<float, false>(t, dr, dm, chunks, (float*)out, s);
+  int status = launch_batch_image(t, sl.dev, nreq, sh, dtype, out, s);
   const cudaError_t er = cudaEventRecord(sl.done, s);
   if (status == ZF_OK && er != cudaSuccess) status = (int)er;
   return status;
 }
 
 }  // namespace zf
+
+// A batch whose image stays resident on the handle's device: re-filling it is
+// a single launch with no host work (zigfast_b200.h: zf_batch_create).
+struct zf_batch {
+  const zf_tables* t;
+  int nreq;
+  int dtype;
+  zf::BatchShape shape;
+  unsigned char* image;  // device
+};
+
+namespace zf {
+
+int batch_create(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
+                 zf_batch** out) {
+  if (nreq < 0 || (nreq > 0 && !reqs)) return ZF_EINVAL;
+  if (t->kind != kKindModified) return ZF_ETABLE;
+  BatchShape sh;
+  ZF_TRY_STATUS(batch_shape(reqs, nreq, dtype, &sh));
+  std::vector<unsigned char> host(std::max<size_t>(sh.bytes(nreq), 16));
+  batch_write(reqs, nreq, sh, host.data());
+  unsigned char* dev = nullptr;
+  ZF_TRY(cudaMalloc(&dev, host.size()));
+  const cudaError_t e = cudaMemcpy(dev, host.data(), host.size(), cudaMemcpyHostToDevice);
+  zf_batch* b = e == cudaSuccess ? new (std::nothrow) zf_batch{t, nreq, dtype, sh, dev} : nullptr;
+  if (!b) {
+    cudaFree(dev);
+    return e != cudaSuccess ? (int)e : ZF_EINVAL;
+  }
+  *out = b;
+  return ZF_OK;
+}
+
+int batch_fill(const zf_batch* b, void* out, cudaStream_t s) {
+  if (b->shape.chunks == 0) return ZF_OK;
+  return launch_batch_image(b->t, b->image, b->nreq, b->shape, b->dtype, out, s);
+}
+
+int batch_destroy(zf_batch* b) {
+  const cudaError_t e = cudaFree(b->image);
+  delete b;
+  return cuda_status(e);
+}
+
+}  // namespace zf
+
+extern "C" const zf_tables* zf_batch_tables(const zf_batch* b) { return b ? b->t : nullptr; }

@@ -93,6 +93,9 @@ int launch_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t
                 void* out, uint64_t n, int64_t* counters, cudaStream_t s);
 int launch_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, void* out,
                       cudaStream_t s);
+int batch_create(const zf_tables* t, const zf_request* reqs, int nreq, int dtype, zf_batch** out);
+int batch_fill(const zf_batch* b, void* out, cudaStream_t s);
+int batch_destroy(zf_batch* b);
 // launchers (zf_stats.cu)
 int launch_fill_stats(const zf_tables* t, int dist, uint64_t seed, uint64_t ctr_base, uint64_t n,
                       const zf_stats_cfg* cfg, double* partials, unsigned long long* counts,

@@ -184,18 +184,37 @@ def test_batch_staging_ring_reuse(zf, orc, cuda):
     request tables go through the handle's reused pinned/device staging slots
     (which grow with the batch), so every batch must still see its own table."""
     import torch
-    plans, outs = [], []
+    batches, outs = [], []
     for b, m in enumerate((3, 40, 7, 300, 300, 12)):  # grows, shrinks, grows past capacity
         reqs = [("normal" if (i + b) % 3 else "exp", 700 + 97 * i, 1000 * b + i) for i in range(m)]
-        plan = zf.BatchPlan([r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs])
-        plans.append((plan, reqs))
-        outs.append(plan.fill(device=cuda))  # no synchronize between batches
+        out, offs = zf.fill_batch(reqs, device=cuda)  # no synchronize between batches
+        batches.append((reqs, offs))
+        outs.append(out)
     torch.cuda.synchronize(cuda)
-    for (plan, reqs), out in zip(plans, outs):
+    for (reqs, offs), out in zip(batches, outs):
         host = out.cpu().numpy()
-        for (dist, n, seed), off in zip(reqs[::17], plan.offsets[::17]):
+        for (dist, n, seed), off in zip(reqs[::17], offs[::17]):
             want, _, _ = orc.fill_ctr(dist, n, seed=seed)
             assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
+
+
+def test_batch_plan_resident_refills(zf, orc, cuda):
+    """A BatchPlan keeps its request table on the device (zf_batch_create):
+    refills are single launches; every refill (into fresh and reused outputs)
+    equals the individual fills."""
+    import torch
+    reqs = [("exp" if i % 2 else "normal", 8192 if i % 7 else 3000 + i, 50 + i) for i in range(97)]
+    plan = zf.BatchPlan([r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs])
+    first = plan.fill(device=cuda).cpu().numpy()
+    again = torch.full((plan.total,), float("nan"), dtype=torch.float64, device=cuda)
+    for _ in range(3):
+        plan.fill(out=again, device=cuda)
+    host = again.cpu().numpy()
+    for (_, n, _), off in zip(reqs, plan.offsets):  # (padding between requests is not written)
+        assert np.array_equal(bits(first[off:off + n]), bits(host[off:off + n]))
+    for (dist, n, seed), off in zip(reqs, plan.offsets):
+        want, _, _ = orc.fill_ctr(dist, n, seed=seed)
+        assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
 
 
 def test_convenience_api(zf, cuda):
@@ -340,3 +359,50 @@ def test_pageable_numpy_fill_page_locks_in_place(zf, cuda):
     small = np.empty(1 << 16)
     a.fill(small)
     assert small.ctypes.data not in samplers._registered
+
+
+@pytest.mark.parametrize("dist", DISTS)
+def test_full_comparison_many_tiles_per_warp(zf, orc, cuda, dist):
+    """n = 2^26 against the oracle in fp64 and fp32: each warp walks ~9 tiles,
+    so the cross-tile paths (the per-warp queue carried over tiles, rounds of
+    32 from several tiles, queue compaction, cooperative normal rounds) all
+    run many times."""
+    import torch
+    n = 1 << 26
+    want, _, _ = orc.fill_ctr(dist, n, seed=4242, ctr_base=1 << 41)
+    got = sampler(zf, dist, 4242, 1 << 41, device=cuda).fill(n).cpu().numpy()
+    assert_bits_equal(got, bits(want), f"{dist} f64 2^26")
+    g32 = torch.empty(n, dtype=torch.float32, device=cuda)
+    sampler(zf, dist, 4242, 1 << 41, device=cuda).fill(g32)
+    assert np.array_equal(g32.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32))
+
+
+_WAVES_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_1403_6870_b200 as zf
+for cls in (zf.ExpSampler, zf.NormalSampler):
+    x = cls(source=zf.UniformSource.counter(77, 5), device="cuda").fill(1 << 24)
+    print(hashlib.sha256(x.cpu().numpy().tobytes()).hexdigest())
+"""
+
+
+def test_one_wave_grid_many_tiles_per_warp(orc, cuda):
+    """ZF_GRID_WAVES=1 in a fresh process: one resident wave, so every warp
+    carries its queue across ~16 tiles of a 2^24 fill; bit-exact with the
+    oracle."""
+    import hashlib
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    env = dict(os.environ, ZF_GRID_WAVES="1")
+    res = subprocess.run([sys.executable, "-c", _WAVES_SCRIPT, root], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = res.stdout.split()
+    for dist, h in zip(("exp", "normal"), got):
+        want, _, _ = orc.fill_ctr(dist, 1 << 24, seed=77, ctr_base=5)
+        assert h == hashlib.sha256(want.tobytes()).hexdigest(), dist
