@@ -76,7 +76,13 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
 #endif
   return z ^ (z >> 33);
 }
-__host__ __device__ __forceinline__ uint64_t ctr_word(uint64_t z) { return fmix64(z); }
+__host__ __device__ __forceinline__ uint64_t ctr_word(uint64_t z) {
+#if defined(ZF_WORD_MIX13)  // experiment builds: the round-1 word function
+  return mix13(z);
+#else
+  return fmix64(z);
+#endif
+}
 
 // One distribution's pack.  sx has kSlots+2 entries so sx[i+1] is in bounds for
 // every byte i: the fast loop reads it branch-free, and entries past L_max hold

@@ -43,6 +43,9 @@ def main():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the equal-output gate")
+    ap.add_argument("--sustain", type=float, default=0.0,
+                    help="instead of timed reps: run each lib/dist for this many seconds and "
+                         "report the average rate and the energy per sample (NVML)")
     ap.add_argument("--cool", type=float, default=0.0,
                     help="idle seconds before each measurement (keeps the power average low)")
     ap.add_argument("libs", nargs="+")
@@ -69,6 +72,32 @@ def main():
             elif not torch.equal(x, ref) and not a.no_check:
                 bad.add(p)
                 print(f"!! {p} differs from {libs[0][0]} on {dname}", flush=True)
+    if a.sustain:
+        import pynvml as N
+        N.nvmlInit()
+        nvh = N.nvmlDeviceGetHandleByIndex(0)
+        for r in range(a.rounds):
+            for p, L, h in libs:
+                for dname in a.dists.split(","):
+                    d = dists[dname]
+                    time.sleep(max(a.cool, 3.0))
+                    torch.cuda.synchronize()
+                    e0 = N.nvmlDeviceGetTotalEnergyConsumption(nvh)
+                    t0 = time.perf_counter()
+                    k = 0
+                    while time.perf_counter() - t0 < a.sustain:
+                        for _ in range(8):
+                            L.zf_fill(h, d, code, a.seed, 0, out.data_ptr(), n, None, None)
+                        k += 8
+                        torch.cuda.synchronize()
+                    dt = time.perf_counter() - t0
+                    e1 = N.nvmlDeviceGetTotalEnergyConsumption(nvh)
+                    clk = N.nvmlDeviceGetClockInfo(nvh, N.NVML_CLOCK_SM)
+                    print(f"{p.split('/')[-1]:24s} {dname:6s} sustained {a.sustain:.1f}s: "
+                          f"{k * n / dt / 1e9:7.1f} G/s, {(e1 - e0) * 1e-3 / dt:6.1f} W, "
+                          f"{(e1 - e0) * 1e-3 / (k * n) * 1e9:.3f} nJ/sample, sm_mhz {clk}",
+                          flush=True)
+        return
     res = {(p, d): [] for p, _, _ in libs for d in a.dists.split(",")}
     clk = {(p, d): [] for p, _, _ in libs for d in a.dists.split(",")}
     try:
