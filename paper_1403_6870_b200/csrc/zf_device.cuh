@@ -67,7 +67,7 @@ __host__ __device__ __forceinline__ uint64_t mix13(uint64_t z) {
 // (profiles/r02_battery.json).  mix13 stays the word function of the
 // reference's own splitmix64 stream (gid 1, oracle mode).
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !defined(ZF_PLAIN_MUL64)
   z = mul64_chained<0xff51afd7ed558ccdull>(z ^ (z >> 33));
   z = mul64_chained<0xc4ceb9fe1a85ec53ull>(z ^ (z >> 33));
 #else

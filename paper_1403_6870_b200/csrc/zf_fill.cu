@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
 
   LaneCounts lc;
   StoreSink<OutT, VEC> sink{out};
+#if defined(ZF_CHECKS) && ZF_CHECKS
+  sink.n_check = n;
+#endif
   run_tiles<DIST, COUNTED, P2>(P, E, seed, ctr_base, sink, n,
                                (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
                                (uint64_t)gridDim.x * kWarps, queue, lane, lc, late);

@@ -61,6 +61,21 @@ constexpr int kQueueCap = ZF_QUEUE_CAP;
 // per-warp shared words: the queue, then 32 x 16 B of round scratch
 constexpr int kQueueWords = kQueueCap + (ZF_COOP ? 128 : 0);
 
+// ZF_CHECKS=1 (debug builds, tests/test_gpu_checked.py): device-side bounds and
+// protocol checks that trap on violation -- queue slots inside the queue,
+// round-scratch indices inside the warp's 32 records, every store inside the
+// output, the staged pack complete before a round reads it.
+#if defined(ZF_CHECKS) && ZF_CHECKS
+#define ZF_CHECK(cond) \
+  do {                 \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define ZF_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 template <typename OutT>
 struct VecOf;
 template <>
@@ -92,9 +107,15 @@ struct StoreSink {
   using Out = OutT;
   static constexpr int V = VecOf<OutT>::V;
   OutT* __restrict__ out;
+#if defined(ZF_CHECKS) && ZF_CHECKS
+  uint64_t n_check = ~0ull;  // stores must stay below it
+#endif
   // pass 1: V consecutive values at k (exceptional ones are NaN placeholders,
   // overwritten in pass 2 while the line is still in L2)
   __device__ __forceinline__ void put_vec(uint64_t k, const OutT* v, uint32_t /*exc_bits*/) {
+#if defined(ZF_CHECKS) && ZF_CHECKS
+    ZF_CHECK(k + V <= n_check);
+#endif
     if constexpr (VEC) {
       *reinterpret_cast<typename VecOf<OutT>::T*>(out + k) = VecOf<OutT>::make(v);
     } else {
@@ -102,7 +123,12 @@ struct StoreSink {
       for (int e = 0; e < V; ++e) out[k + e] = v[e];
     }
   }
-  __device__ __forceinline__ void put(uint64_t k, OutT v, bool /*exc*/) { out[k] = v; }
+  __device__ __forceinline__ void put(uint64_t k, OutT v, bool /*exc*/) {
+#if defined(ZF_CHECKS) && ZF_CHECKS
+    ZF_CHECK(k < n_check);
+#endif
+    out[k] = v;
+  }
   __device__ __forceinline__ void flag(uint32_t& mask, double d, uint32_t bit) {
     or_if_nan(mask, d, bit);
   }
@@ -396,6 +422,7 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
     const int r = __popc(un);
     const int rank = __popc(un & lt);  // my slot if unresolved
     // owners publish (stream base, slot j, next attempt) at their rank
+    ZF_CHECK(r >= 1 && r <= 32 && rank < 32);
     if (!done)
       reinterpret_cast<uint4*>(own)[rank] =
           make_uint4((uint32_t)sbase, (uint32_t)(sbase >> 32), (uint32_t)j, next);
@@ -403,6 +430,7 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
     // lane / r and lane % r without an integer division: (lane + 0.5) / r is
     // at least 1/64 away from an integer, far above the reciprocal's error
     const int qd = __float2int_rz(__fmul_rn((float)lane + 0.5f, __frcp_rn((float)r)));
+    ZF_CHECK(lane - qd * r >= 0 && lane - qd * r < r);
     const uint4 st4 = reinterpret_cast<const uint4*>(own)[lane - qd * r];
     __syncwarp();
     const uint64_t sb = ((uint64_t)st4.y << 32) | st4.x;
@@ -503,6 +531,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       mbar_wait(late, 0);
       tables_ready = true;
     }
+    ZF_CHECK(P.nslots == P.lmax + 1 && E.nslots == E.lmax + 1);  // the whole pack landed
   };
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   // queue entry = tile iteration << kTileBits | lane * kPerLane | mask bit: the
@@ -570,7 +599,8 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
             for (uint32_t m = drop_top(m2); m;) {
               const int b = 31 - __clz(m);
               m ^= 1u << b;
-              q[slot++] = tag | (uint32_t)b;
+              ZF_CHECK(slot < kQueueCap);
+            q[slot++] = tag | (uint32_t)b;
             }
           }
           } else {
@@ -578,12 +608,14 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
           for (uint32_t m = drop_top(mask); m;) {
             const int b = 31 - __clz(m);
             m ^= 1u << b;
+            ZF_CHECK(slot < kQueueCap);
             q[slot++] = tag | (uint32_t)b;
           }
           }
         }
       }
       qn += total;
+      ZF_CHECK(qn <= kQueueCap && slot <= qn);
       __syncwarp();
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 2  // cost isolation: scan + enqueue, no rounds
       if (qn >= 32) qn = 0;

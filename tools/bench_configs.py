@@ -8,9 +8,9 @@ c1   oracle mode: Exponential / N(0,1) fp64, n = 1e6 from UniformSource(42)
 c1big  the same pipeline at n = 2^26 (throughput of oracle mode)
 c4   4096 requests x 8192 samples, alternating exp/normal, seeds 0..4095:
      one batched launch vs 4096 separate fills
-c5   tail stress, one GPU's share of config 5: N(0,1) n = 2^33, seed 99, counts of
-     |x| > 5, 6, 7 and Exp(1) n = 2^33 counts of x > X[1], vs analytic tail mass
-     (5-sigma binomial); generate-and-count, nothing materialised
+c5   tail stress, config 5 in full on one GPU: N(0,1) and Exp(1), 2^36 each, seed
+     99, counts of |x| > 5, 6, 7 and of x > X[1] vs the analytic tail mass
+     (5-sigma binomial); generate-and-count, nothing materialised (scale.config5)
 f32  fp32 production fills (n = 2^28) for both distributions
 trad modified vs traditional ziggurat on the GPU (the paper's Table 1 comparison,
      reference tests/test_acceptance.py criterion 6): fp64 fills n = 2^28 and
@@ -109,25 +109,29 @@ def c4():
                   "fills through the Python API"})
 
 
-def c5(n=1 << 33):
-    s = zf.NormalSampler(source=zf.UniformSource.counter(99), device=dev)
+def c5(total=1 << 36):
+    """Config 5 on one GPU (the whole 2^36 per distribution; under torchrun the
+    same scale.config5 call splits it over the ranks): generate-and-count in
+    the tail-only kernel mode (moments = 0, thresholds above every fast-path
+    value), with the full-statistics kernel timed beside it for the record."""
+    from paper_1403_6870_b200 import scale
+    scale.config5(1 << 24, 0, 1, device=dev)  # warm
+    torch.cuda.synchronize()
     t = time.perf_counter()
-    _, res = quality.device_sums(s, n, thresholds=(5.0, 6.0, 7.0), abs_thresh=True)
+    rep = scale.config5(total, 0, 1, device=dev)
     torch.cuda.synchronize()
     sec = time.perf_counter() - t
-    rows = []
-    for th, c in zip((5.0, 6.0, 7.0), res.thresh_counts):
-        p = math.erfc(th / math.sqrt(2.0))
-        ok, mean, sd = quality.binomial_check(c, n, p)
-        rows.append({"threshold": th, "count": c, "expected": mean, "sd": sd, "within_5sigma": ok})
-    x1 = float(zf.default_tables("exponential").x[1])
-    se = zf.ExpSampler(source=zf.UniformSource.counter(99), device=dev)
-    _, rese = quality.device_sums(se, n, thresholds=(x1,))
-    ok, mean, sd = quality.binomial_check(rese.thresh_counts[0], n, math.exp(-x1))
-    emit({"config": "c5 (one GPU's share: 2^33 of 2^36)", "n": n, "seconds_normal": sec,
-          "samples_per_s_generate_and_count": n / sec, "normal_tails": rows,
-          "exp_tail_beyond_X1": {"X1": x1, "count": rese.thresh_counts[0], "expected": mean,
-                                 "sd": sd, "within_5sigma": ok}})
+    n = 1 << 33
+    s = zf.NormalSampler(source=zf.UniformSource.counter(99), device=dev)
+    t = time.perf_counter()
+    quality.device_sums(s, n, thresholds=(5.0, 6.0, 7.0), abs_thresh=True)
+    torch.cuda.synchronize()
+    full = time.perf_counter() - t
+    emit({"config": "c5", "n_total_per_dist": total, "seconds": sec,
+          "samples_per_s": 2 * total / sec, **rep,
+          "full_statistics_kernel_2p33_samples_per_s": n / full,
+          "note": "normal |x| > 5, 6, 7 and Exp(1) x > X[1]: tail-only kernel (counts on the "
+                  "rare path only) vs the full moments + thresholds kernel on 2^33 normal draws"})
 
 
 def f32(n=1 << 28):
