@@ -398,3 +398,13 @@ int batch_destroy(zf_batch* b) {
 }  // namespace zf
 
 extern "C" const zf_tables* zf_batch_tables(const zf_batch* b) { return b ? b->t : nullptr; }
+
+#if defined(ZF_CHECKS) && ZF_CHECKS
+// debug builds: the first failed ZF_CHECK of this file's kernels (0 = none); resets it
+extern "C" unsigned int zf_debug_check_line_fill(void) {
+  unsigned int v = 0, z = 0;
+  cudaMemcpyFromSymbol(&v, zf::zf_check_line, sizeof v);
+  cudaMemcpyToSymbol(zf::zf_check_line, &z, sizeof z);
+  return v;
+}
+#endif

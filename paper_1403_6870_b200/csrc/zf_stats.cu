@@ -291,3 +291,13 @@ int launch_stats(int dtype, const void* x, uint64_t n, const zf_stats_cfg* cfg, 
 }
 
 }  // namespace zf
+
+#if defined(ZF_CHECKS) && ZF_CHECKS
+// debug builds: the first failed ZF_CHECK of this file's kernels (0 = none); resets it
+extern "C" unsigned int zf_debug_check_line_stats(void) {
+  unsigned int v = 0, z = 0;
+  cudaMemcpyFromSymbol(&v, zf::zf_check_line, sizeof v);
+  cudaMemcpyToSymbol(zf::zf_check_line, &z, sizeof z);
+  return v;
+}
+#endif

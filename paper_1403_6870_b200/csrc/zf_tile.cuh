@@ -62,13 +62,16 @@ constexpr int kQueueCap = ZF_QUEUE_CAP;
 constexpr int kQueueWords = kQueueCap + (ZF_COOP ? 128 : 0);
 
 // ZF_CHECKS=1 (debug builds, tests/test_gpu_checked.py): device-side bounds and
-// protocol checks that trap on violation -- queue slots inside the queue,
-// round-scratch indices inside the warp's 32 records, every store inside the
-// output, the staged pack complete before a round reads it.
+// protocol checks -- queue slots inside the queue, round-scratch indices
+// inside the warp's 32 records, every store inside the output, the staged
+// pack complete before a round reads it.  A failed check records its source
+// line in zf_check_line (one per translation unit, read back by
+// zf_debug_check_line_*) and the kernel carries on.
 #if defined(ZF_CHECKS) && ZF_CHECKS
-#define ZF_CHECK(cond) \
-  do {                 \
-    if (!(cond)) __trap(); \
+static __device__ unsigned int zf_check_line;
+#define ZF_CHECK(cond)                                  \
+  do {                                                  \
+    if (!(cond)) atomicCAS(&zf_check_line, 0u, __LINE__); \
   } while (0)
 #else
 #define ZF_CHECK(cond) \
@@ -556,6 +559,9 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       int total;
       bool multi;  // some lane holds two or more exceptions
       int slot = qn + warp_excl_mask(mask, lane, &total, &multi);
+#if defined(ZF_CHECKS) && ZF_CHECKS
+      const int first_slot = slot;  // this lane's entries: [first_slot, + popc(mask))
+#endif
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 1  // cost isolation: scan only
       if (total == 12345) q[lane] = slot;
       continue;
@@ -615,7 +621,9 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         }
       }
       qn += total;
-      ZF_CHECK(qn <= kQueueCap && slot <= qn);
+#if defined(ZF_CHECKS) && ZF_CHECKS
+      ZF_CHECK(qn <= kQueueCap && first_slot + __popc(mask) <= qn);
+#endif
       __syncwarp();
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 2  // cost isolation: scan + enqueue, no rounds
       if (qn >= 32) qn = 0;
