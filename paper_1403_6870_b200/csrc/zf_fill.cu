@@ -103,6 +103,9 @@ struct DevRequest {
 #ifndef ZF_BATCH_WAVES
 #define ZF_BATCH_WAVES 1  // resident waves of the batch kernel
 #endif
+#ifndef ZF_BATCH_PREFETCH
+#define ZF_BATCH_PREFETCH 1  // load the next chunk's request ahead
+#endif
 #ifndef ZF_BATCH_MIN_BLOCKS
 #define ZF_BATCH_MIN_BLOCKS 1
 #endif
@@ -121,9 +124,20 @@ __global__ void __launch_bounds__(kThreads, ZF_BATCH_MIN_BLOCKS)
   __syncthreads();
   LaneCounts lc;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t chunk = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); chunk < total_chunks;
-       chunk += nw) {
+  uint64_t chunk = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+#if ZF_BATCH_PREFETCH
+  // the next chunk's request is loaded while this one runs (two dependent
+  // global loads per chunk would otherwise stall the warp before pass 1)
+  DevRequest nr{};
+  if (chunk < total_chunks) nr = reqs[__ldg(chunk_req + chunk)];
+#endif
+  for (; chunk < total_chunks; chunk += nw) {
+#if ZF_BATCH_PREFETCH
+    const DevRequest r = nr;
+    if (chunk + nw < total_chunks) nr = reqs[__ldg(chunk_req + chunk + nw)];
+#else
     const DevRequest r = reqs[__ldg(chunk_req + chunk)];
+#endif
     const uint64_t t0 = (chunk - r.chunk_begin) * kBatchChunk;
     // tiles [t0, t0 + kBatchChunk) of the request: cap n at the chunk's end
     const uint64_t n_eff = std::min<uint64_t>(r.n, (t0 + kBatchChunk) * kTile);

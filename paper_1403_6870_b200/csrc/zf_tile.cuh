@@ -263,8 +263,24 @@ __device__ __forceinline__ uint32_t fast_pass(const DevPack& P, uint64_t seed, u
         // sx[i+1] is NaN for every byte i >= L_max (see fill_devpack), so the
         // fast value itself flags an exceptional sample: a DSETP on the fp64
         // pipe instead of integer compare/select work on the busy ALU pipe.
+#if defined(ZF_DEBUG_P1)  // energy isolation builds (run with ZF_PASS2=9): drop one stage
+        // 1: no word function (the counter itself)  2: no table lookup
+        // 3: no conversion + multiply (word bits stored)  4: constant stores only
+        const uint64_t z = st + (uint64_t)e * kGamma;
+        const uint64_t w = ZF_DEBUG_P1 == 1 || ZF_DEBUG_P1 == 4 ? z : ctr_word(z);
+        double d;
+        if (ZF_DEBUG_P1 == 2)
+          d = __dmul_rn(__ll2double_rn((long long)w), 0x1p-63);
+        else if (ZF_DEBUG_P1 == 3)
+          d = __longlong_as_double((long long)(w & 0x3fffffffffffffffull)) + sx[(w & 0xFF) + 1];
+        else if (ZF_DEBUG_P1 == 4)
+          d = (double)e;
+        else
+          d = fast_value<DIST>(sx, w);
+#else
         const uint64_t w = ctr_word(st + (uint64_t)e * kGamma);
         double d = fast_value<DIST>(sx, w);
+#endif
         if constexpr (kTrad<DIST>)  // traditional: integer fast-accept test
           d = trad_fast<DIST>(P.kk, w) ? d : __longlong_as_double(0x7ff8000000000000ll);
         sink.flag(mask, d, 1u << (it * V + e));
