@@ -206,13 +206,7 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
     if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
     if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
   }
-  size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
-  // ZF_OCC=c (experiments): pad the shared-memory request so at most c CTAs fit per SM
-  static const int env_occ = [] {
-    const char* e = getenv("ZF_OCC");
-    return e ? std::max(1, atoi(e)) : 0;
-  }();
-  if (env_occ) smem = std::max<size_t>(smem, (size_t)(220 * 1024) / (size_t)env_occ - 4096);
+  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));
   kernel<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
