@@ -445,30 +445,38 @@ constexpr int kXoBits = 8;      // jump-table radix 256: <= 3 polynomials for 2^
 constexpr int kXoRadix = 1 << kXoBits;
 constexpr int kXoLevels = 5;    // base-256 digits of the thread index (2^40 threads)
 
-// the jump table for B = kXoBlock, built once on the host and kept on every
-// device that used it (40 KB)
-const uint64_t* jump_table_device() {
-  static std::vector<uint64_t> host = [] {
-    std::vector<uint64_t> p((size_t)kXoLevels * (kXoRadix - 1) * 4, 0);
-    xoshiro_radix_polys(kXoBlock, kXoBits, kXoLevels, p.data());
-    return p;
-  }();
+// Short windows use 64-word blocks: 16x the threads, so the per-thread jump
+// (a latency-bound chain of up to 3 x 256 generator steps) and the sequential
+// block walk both shrink -- 1.1 M words took 46 us with 1024-word blocks.
+constexpr int kXoBlockShort = 64;
+constexpr uint64_t kXoShortMax = 1ull << 22;  // windows up to this many words
+
+// the jump table for blocks of B words, built once per B on the host and kept
+// on every device that used it (40 KB each)
+const uint64_t* jump_table_device(int B = kXoBlock) {
   static std::mutex mu;
-  static std::vector<uint64_t*> per_device(64, nullptr);
+  static std::vector<uint64_t> host[2];
+  static std::vector<uint64_t*> per_device[2] = {std::vector<uint64_t*>(64, nullptr),
+                                                 std::vector<uint64_t*>(64, nullptr)};
+  const int which = B == kXoBlock ? 0 : 1;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  if (!per_device[dev]) {
+  if (host[which].empty()) {
+    host[which].assign((size_t)kXoLevels * (kXoRadix - 1) * 4, 0);
+    xoshiro_radix_polys((uint64_t)B, kXoBits, kXoLevels, host[which].data());
+  }
+  if (!per_device[which][dev]) {
     uint64_t* d = nullptr;
-    if (cudaMalloc(&d, host.size() * sizeof(uint64_t)) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice) !=
-        cudaSuccess) {
+    const size_t bytes = host[which].size() * sizeof(uint64_t);
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, host[which].data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
       cudaFree(d);
       return nullptr;
     }
-    per_device[dev] = d;
+    per_device[which][dev] = d;
   }
-  return per_device[dev];
+  return per_device[which][dev];
 }
 
 
@@ -509,8 +517,9 @@ __device__ __forceinline__ void xo_jump_to(const uint64_t* __restrict__ table, u
 }
 
 // thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0, one jump
-// polynomial x^(d*16^r*B) per nonzero base-16 digit d of t; output staged
+// polynomial x^(d*256^r*B) per nonzero base-256 digit d of t; output staged
 // through a 32x32 smem tile per warp so stores are coalesced rows.
+template <int B>
 __global__ void __launch_bounds__(128)
     words_xoshiro(ulonglong4 s0, const uint64_t* __restrict__ polys, uint64_t n,
                   uint64_t* __restrict__ out) {
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(128)
   uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
   xo_jump_to(polys, t, s);
   const uint64_t warp_first = t - lane;  // thread index of lane 0
-  for (int c = 0; c < kXoBlock; c += 32) {
+  for (int c = 0; c < B; c += 32) {
 #pragma unroll 4
     for (int j = 0; j < 32; ++j) {
       tile[wid][lane][j] = ((s[0] + s[3]) << 23 | (s[0] + s[3]) >> 41) + s[0];
@@ -528,7 +537,7 @@ __global__ void __launch_bounds__(128)
     }
     __syncwarp();
     for (int r = 0; r < 32; ++r) {  // row r = lane r's 32 consecutive words
-      const uint64_t idx = (warp_first + r) * kXoBlock + c + lane;
+      const uint64_t idx = (warp_first + r) * B + c + lane;
       if (idx < n) out[idx] = tile[wid][r][lane];
     }
     __syncwarp();
@@ -921,14 +930,19 @@ int launch_words(int gid, const uint64_t* state, uint64_t n, uint64_t* out, cuda
     return cuda_status(cudaGetLastError());
   }
   if (gid != ZF_GEN_XOSHIRO256PP) return ZF_EDIST;
-  const uint64_t threads = (n + kXoBlock - 1) / kXoBlock;
+  const bool shrt = n <= kXoShortMax;
+  const int B = shrt ? kXoBlockShort : kXoBlock;
+  const uint64_t threads = (n + B - 1) / B;
   if (threads - 1 >= (1ull << (kXoBits * kXoLevels))) return ZF_ERANGE;
-  const uint64_t* dpolys = jump_table_device();
+  const uint64_t* dpolys = jump_table_device(B);
   if (!dpolys) return ZF_EDEVICE;
   const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
   // round the grid to whole warps so every warp's smem tile is full
   const uint64_t blocks = (threads + 127) / 128;
-  words_xoshiro<<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
+  if (shrt)
+    words_xoshiro<kXoBlockShort><<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
+  else
+    words_xoshiro<kXoBlock><<<(uint32_t)blocks, 128, 0, s>>>(s0, dpolys, n, out);
   return cuda_status(cudaGetLastError());
 }
 

@@ -1,3 +1,4 @@
-V=build/variants
-ZF_PASS2=9 timeout 900 python tools/ab.py --no-check --sustain 2.0 --rounds 1 --n 30 --dists normal $V/cur.so $V/p1d1.so $V/p1d2.so $V/p1d3.so $V/p1d4.so > gpurun_out/ab16_energy.txt 2>&1
-ZF_PASS2=9 timeout 300 python tools/ab.py --no-check --cool 0.15 --n 28 --reps 6 --rounds 4 --dists normal $V/cur.so $V/p1d1.so $V/p1d2.so $V/p1d3.so $V/p1d4.so > gpurun_out/ab16_cold.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_oracle_mode.py tests/test_gpu_traditional.py -q -x > gpurun_out/om_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/om_tests.txt
+python tools/oracle_prof.py 20 20 exp > gpurun_out/c1_plain.txt 2>&1
+python tools/oracle_prof.py 20 20 normal >> gpurun_out/c1_plain.txt 2>&1
+timeout 300 python tools/bench_configs.py c1 >> gpurun_out/c1_plain.txt 2>&1
