@@ -257,6 +257,13 @@ int zf_batch_fill(const zf_batch* b, void* out_dev, void* stream);
 int zf_batch_destroy(zf_batch* b);
 const zf_tables* zf_batch_tables(const zf_batch* b);
 
+/* Page-lock (and release) a caller-owned host buffer in place, so fills into
+ * it DMA at the link rate: how the Python layer serves `fill(np.empty(n))`
+ * (the reference's pageable-array usage, exponential.py:45-50) without a
+ * staging copy.  A failed registration leaves no CUDA last-error behind. */
+int zf_host_register(void* ptr, uint64_t bytes);
+int zf_host_unregister(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

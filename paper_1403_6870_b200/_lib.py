@@ -32,7 +32,7 @@ EXPORTS = (
     "zf_xoshiro_jump", "zf_xoshiro_pow2_poly", "zf_fill_batch", "zf_trad_tables_create",
     "zf_format_g17", "zf_format_scratch_words", "zf_tables_create_default",
     "zf_trad_tables_create_default", "zf_batch_create", "zf_batch_fill", "zf_batch_destroy",
-    "zf_batch_tables",
+    "zf_batch_tables", "zf_host_register", "zf_host_unregister",
 )
 EXP, NORMAL, TRAD_EXP, TRAD_NORMAL = 0, 1, 2, 3
 
@@ -108,6 +108,8 @@ def lib():
                 "zf_batch_fill": (i32, [vp, vp, vp]),
                 "zf_batch_destroy": (i32, [vp]),
                 "zf_batch_tables": (vp, [vp]),
+                "zf_host_register": (i32, [vp, u64]),
+                "zf_host_unregister": (i32, [vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -340,6 +340,20 @@ int zf_fill_batch(const zf_tables* t, const zf_request* reqs, int nreq, int dtyp
   return launch_fill_batch(t, reqs, nreq, dtype, out_dev, as_stream(stream));
 }
 
+int zf_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return ZF_EINVAL;
+  const cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) cudaGetLastError();  // not sticky: leave no last-error behind
+  return cuda_status(e);
+}
+
+int zf_host_unregister(void* ptr) {
+  if (!ptr) return ZF_EINVAL;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) cudaGetLastError();
+  return cuda_status(e);
+}
+
 int zf_batch_create(const zf_tables* t, const zf_request* reqs, int nreq, int dtype,
                     zf_batch** out) {
   if (!t || !out) return ZF_EINVAL;

@@ -78,8 +78,7 @@ def _unregister(ptr: int) -> None:
         entry = _registered.pop(ptr, None)
     if entry is not None:
         try:
-            import torch
-            torch.cuda.cudart().cudaHostUnregister(ptr)
+            _lib.lib().zf_host_unregister(ptr)
         except Exception:  # interpreter shutdown
             pass
 
@@ -100,7 +99,6 @@ def _page_locked(arr) -> bool:
     owner = _owner(arr)
     if owner is None:
         return False
-    import torch
     ptr, nbytes = owner.ctypes.data, owner.nbytes
     evict = []
     with _reg_lock:
@@ -117,9 +115,8 @@ def _page_locked(arr) -> bool:
     for p, fin in evict:
         fin.detach()
         _unregister(p)
-    rc = torch.cuda.cudart().cudaHostRegister(ptr, nbytes, 0)
-    if int(getattr(rc, "value", rc)) != 0:
-        return False
+    if _lib.lib().zf_host_register(ptr, nbytes) != 0:
+        return False  # e.g. another thread registered it first: stage instead
     with _reg_lock:
         _registered[ptr] = (nbytes, weakref.finalize(owner, _unregister, ptr))
     return True
