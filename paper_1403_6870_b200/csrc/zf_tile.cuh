@@ -48,6 +48,11 @@ constexpr int kPass1Unroll = ZF_PASS1_UNROLL;
 #ifndef ZF_ASYNC_STAGE
 #define ZF_ASYNC_STAGE 1
 #endif
+// Normal rounds: a tail sample's first Marsaglia attempt from the words the
+// box attempt already computed (see resolve_round_normal).
+#ifndef ZF_TAILFAST
+#define ZF_TAILFAST 1
+#endif
 
 #ifndef ZF_QUEUE_CAP
 #define ZF_QUEUE_CAP 128
@@ -407,9 +412,22 @@ __device__ __forceinline__ void resolve_round_normal(const DevPack& P, const Dev
   const int j = alias_from(P, w1, w2);
   uint32_t next = 1;  // this lane's sample: attempts 0 .. next-1 all rejected
   if (j == 0) {
-    NoCount c;
-    CtrStream s{sbase + 2 * kGamma};
-    val = normal_tail(P, E, s, c);
+#if ZF_TAILFAST
+    // Marsaglia's first attempt from words 3 and 4 (already computed for the
+    // box attempt) when both embedded exponential draws take their fast path
+    // -- the common case, the same arithmetic as normal_tail; anything else
+    // (an exceptional byte: NaN, or a rejection) runs the full loop
+    const double e1 = fast_value<ZF_EXP>(E.sx, w3), e2 = fast_value<ZF_EXP>(E.sx, w4);
+    const double x = __ddiv_rn(e1, P.tailx);
+    if (__dadd_rn(e2, e2) > __dmul_rn(x, x)) {
+      val = __dadd_rn(P.tailx, x);
+    } else
+#endif
+    {
+      NoCount c;
+      CtrStream s{sbase + 2 * kGamma};
+      val = normal_tail(P, E, s, c);
+    }
     done = true;
   } else {
     done = normal_box_words(P, j, w3, w4, val);
