@@ -42,7 +42,7 @@ constexpr int default_pass2() {
 #endif
 
 template <int DIST, typename OutT, bool COUNTED, bool VEC, int P2>
-__global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
+__global__ void __launch_bounds__(kFillThreads, ZF_MIN_BLOCKS)
     fill_ctr_kernel(const DevTables* __restrict__ gt, uint64_t seed, uint64_t ctr_base,
                     OutT* __restrict__ out, uint64_t n, unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(kThreads, ZF_MIN_BLOCKS)
   sink.n_check = n;
 #endif
   run_tiles<DIST, COUNTED, P2>(P, E, seed, ctr_base, sink, n,
-                               (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5),
-                               (uint64_t)gridDim.x * kWarps, queue, lane, lc, late);
+                               (uint64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5),
+                               (uint64_t)gridDim.x * kFillWarps, queue, lane, lc, late);
   if (COUNTED) flush_counts(lc, counters);
 }
 
@@ -157,31 +157,38 @@ __global__ void __launch_bounds__(kThreads, ZF_BATCH_MIN_BLOCKS)
 
 template <typename K>
 static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid,
-                    int fixed_waves = 0) {
+                    int fixed_waves = 0, int threads = kThreads) {
   static_assert(sizeof(K) > 0, "");
   int per_sm = 0;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return (int)e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   if (e != cudaSuccess) return (int)e;
   per_sm = std::max(per_sm, 1);
-  const uint64_t want = (ntiles + kWarps - 1) / kWarps;
-  // ZF_GRID_WAVES=w overrides the number of resident waves per launch; by
-  // default it grows with the fill (measured on B200, normal / exp G/s at the
-  // chosen value vs 4 waves: 2^26 samples 4 waves; 2^28 6 waves, 633 / 663 vs
-  // 624 / 659; 2^30 8 waves, 629 / 637 vs 605 / 630; 2^32 12 waves, 631 / 656
-  // vs 602 / 622 -- tools/ab_waves_n.sh)
+  const uint64_t want = (ntiles + threads / 32 - 1) / (threads / 32);
+  // ZF_GRID_WAVES=w overrides the number of resident waves per launch.  By
+  // default every warp gets ~kTilesPerWarp tiles: a warp that walks hundreds
+  // of grid-strided tiles drifts away from the other resident warps, and the
+  // write front spreads over more DRAM pages; many short-lived CTAs pay for
+  // their table staging and drain.  Measured on B200 (tools/ab_waves_sweep.sh,
+  // normal / exp G samples/s, tiles per warp in brackets): 2^32 samples 12
+  // waves 735 / 773 (295), 48 waves 755 / 794 (74), 192 waves 727 / 773 (18);
+  // 2^30 8 waves 713 / 764 (110), 12 waves 739 / 787 (74); 2^28 3-6 waves
+  // 720 / 764 (74-37), 8 waves 711 / 760; 2^26 1 wave 660 / 701, 4 waves
+  // 645 / 694.
+  constexpr uint64_t kTilesPerWarp = 64;
   static const int env_waves = [] {
     const char* e = getenv("ZF_GRID_WAVES");
     return e ? std::max(1, atoi(e)) : 0;
   }();
-  const int waves = fixed_waves ? fixed_waves
-                    : env_waves ? env_waves
-                    : ntiles <= (1ull << 17) ? 4
-                    : ntiles <= (1ull << 19) ? 6
-                    : ntiles <= (1ull << 21) ? 8
-                                             : 12;
+  const uint64_t resident_warps = (uint64_t)per_sm * sm_count * (threads / 32);
+  const int waves =
+      fixed_waves ? fixed_waves
+      : env_waves ? env_waves
+                  : (int)std::max<uint64_t>(
+                        1, (ntiles + resident_warps * kTilesPerWarp / 2) /
+                               (resident_warps * kTilesPerWarp));
   *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count * waves);
   if (*grid < 1) *grid = 1;
   return ZF_OK;
@@ -206,10 +213,15 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
     if (p2 == 3) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 3>;
     if (p2 == 9) kernel = fill_ctr_kernel<DIST, OutT, false, VEC, 9>;
   }
-  const size_t smem = kPacks * sizeof(DevPack) + (size_t)kWarps * kQueueWords * sizeof(uint32_t);
+#ifndef ZF_SMEM_PAD
+#define ZF_SMEM_PAD 0  // experiment builds: extra shared memory per CTA (limits CTAs per SM)
+#endif
+  const size_t smem = kPacks * sizeof(DevPack) +
+                      (size_t)kFillWarps * kQueueWords * sizeof(uint32_t) + ZF_SMEM_PAD;
   int grid = 0;
-  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid));
-  kernel<<<grid, kThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
+  ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid, 0,
+                         kFillThreads));
+  kernel<<<grid, kFillThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
   return cuda_status(cudaGetLastError());
 }
 

@@ -22,6 +22,13 @@ namespace zf {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+// CTA size of the production fill kernel (a warp count that is not a power of
+// two lets more 84-88-register warps fit on an SM)
+#ifndef ZF_FILL_THREADS
+#define ZF_FILL_THREADS 256
+#endif
+constexpr int kFillThreads = ZF_FILL_THREADS;
+constexpr int kFillWarps = kFillThreads / 32;
 #ifndef ZF_PER_LANE
 #define ZF_PER_LANE 16
 #endif
