@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kRT)
 template <int DIST>
 __global__ void __launch_bounds__(kRT)
     rp_compact_exc(Window win, const DevPack* __restrict__ P, const uint32_t* __restrict__ boff,
-                   uint32_t* __restrict__ E) {
+                   uint32_t* __restrict__ E, uint32_t cap) {
   __shared__ uint32_t wb[kRT / 32];
   const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
   uint64_t w[kRI];
@@ -198,7 +198,10 @@ __global__ void __launch_bounds__(kRT)
   uint32_t o = boff[blockIdx.x] + warp_base(c, wb, nullptr);
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    if ((b[j] >> (threadIdx.x & 31)) & 1) E[o + __popc(b[j] & lt)] = (uint32_t)striped_pos(j);
+    if ((b[j] >> (threadIdx.x & 31)) & 1) {
+      const uint32_t e = o + __popc(b[j] & lt);
+      if (e < cap) E[e] = (uint32_t)striped_pos(j);  // (the host sized E for a bound)
+    }
     o += __popc(b[j]);
   }
 }
@@ -214,14 +217,14 @@ struct ExcOut {
 template <int DIST>
 __global__ void __launch_bounds__(kRT)
     rp_draw_exc(const DevTables* __restrict__ gt, Window win, const uint32_t* __restrict__ E,
-                uint32_t m, ExcOut o) {
+                const uint32_t* __restrict__ pm, ExcOut o) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kPacks = kPacksOf<DIST>;
   DevPack* sp = reinterpret_cast<DevPack*>(smem_raw);
   stage_block(sp, primary_pack<DIST>(gt), kPacks * (int)sizeof(DevPack));
   __syncthreads();
   const uint32_t i = blockIdx.x * kRT + threadIdx.x;
-  if (i >= m) return;
+  if (i >= *pm) return;
   const uint64_t p = E[i];
   BufStream s{win.w, win.nwords, win.cursor, p + 1, win.L, 0, false};
   const uint64_t u = win.word(p);
@@ -241,8 +244,9 @@ __device__ __forceinline__ uint64_t reach_of(const uint32_t* E, const uint32_t* 
 }
 
 __global__ void rp_reach_max(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
-                             uint32_t m, uint64_t* __restrict__ bmax) {
+                             const uint32_t* __restrict__ pm, uint64_t* __restrict__ bmax) {
   __shared__ uint64_t wb[32];
+  const uint32_t m = *pm;
   const uint64_t i0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
   uint64_t mx = 0;
   for (int j = 0; j < kRI; ++j)
@@ -253,8 +257,10 @@ __global__ void rp_reach_max(const uint32_t* __restrict__ E, const uint32_t* __r
 }
 
 __global__ void rp_heads(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
-                         uint32_t m, const uint64_t* __restrict__ bpre, uint8_t* __restrict__ head) {
+                         const uint32_t* __restrict__ pm, const uint64_t* __restrict__ bpre,
+                         uint8_t* __restrict__ head) {
   __shared__ uint64_t wb[32];
+  const uint32_t m = *pm;
   const uint64_t i0 = (uint64_t)blockIdx.x * kRB + (uint64_t)threadIdx.x * kRI;
   uint64_t mx = 0;
   for (int j = 0; j < kRI; ++j)
@@ -271,7 +277,9 @@ __global__ void rp_heads(const uint32_t* __restrict__ E, const uint32_t* __restr
 constexpr int kWalkChunk = 16;
 
 __global__ void rp_walk(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
-                        const uint8_t* __restrict__ head, uint32_t m, uint8_t* __restrict__ real) {
+                        const uint8_t* __restrict__ head, const uint32_t* __restrict__ pm,
+                        uint8_t* __restrict__ real) {
+  const uint32_t m = *pm;
   const uint64_t beg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kWalkChunk;
   if (beg >= m) return;
   const uint64_t end = std::min<uint64_t>(beg + kWalkChunk, m);
@@ -290,10 +298,11 @@ __global__ void rp_walk(const uint32_t* __restrict__ E, const uint32_t* __restri
 // mark the interior words of every real draw, and count them per emit block
 // (real draws never overlap, so the counts are exact)
 __global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
-                        const uint8_t* __restrict__ real, uint32_t m, uint64_t L,
-                        uint8_t* __restrict__ interior, uint32_t* __restrict__ block_int) {
+                        const uint8_t* __restrict__ real, const uint32_t* __restrict__ pm,
+                        uint64_t L, uint8_t* __restrict__ interior,
+                        uint32_t* __restrict__ block_int) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m || !real[i]) return;
+  if (i >= *pm || !real[i]) return;
   const uint64_t p = E[i];
   const uint64_t stop = len[i] == kIncomplete ? L : std::min<uint64_t>(p + len[i], L);
   for (uint64_t q = p + 1; q < stop; ++q) interior[q] = 1;
@@ -326,34 +335,42 @@ struct EmitArgs {
   uint64_t n;
   zf_path_rec* recs;
   unsigned long long* counters;  // internal [6]
-  unsigned long long* consumed;  // internal scalar
+  unsigned long long* consumed;  // internal scalar: words consumed + 1 (0: n not reached)
   uint32_t boff_stride;          // boff_exc entries per emit block (1, or 2 with segments)
 };
 
 #ifndef ZF_EMIT_MINB
 #define ZF_EMIT_MINB 6  // 40 registers: occupancy hides the load latency
 #endif
-template <int DIST, typename OutT>
-__global__ void __launch_bounds__(kRT, ZF_EMIT_MINB)
+// FULL = false: plain fills (no path records, no counters) -- the default
+// oracle-mode call; its per-position code keeps no counter or record state.
+// Positions are 32-bit (windows are < 2^32 positions, run_generated/replay_typed).
+template <int DIST, typename OutT, bool FULL>
+__global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
     rp_emit(const DevTables* __restrict__ gt, Window win, EmitArgs a, OutT* __restrict__ out) {
   __shared__ uint2 wb[kRT / 32];
   const DevPack* P = primary_pack<DIST>(gt);
   const double* sx = P->sx;  // 2 KB, L1-resident: no per-block staging barrier
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t L32 = (uint32_t)win.L;
+  const uint32_t p0 = (uint32_t)striped_pos(0);  // this thread's item j is p0 + 32 j
+  // the block's offsets do not depend on the words: in flight with them
+  const uint32_t boff_e = __ldg(a.boff_exc + (uint64_t)blockIdx.x * a.boff_stride);
+  const uint32_t boff_s = __ldg(a.boff_start + blockIdx.x);
   uint64_t wds[kRI];
   uint8_t inter[kRI];
   load_striped(win, wds);
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const uint64_t p = striped_pos(j);
-    inter[j] = p < win.L ? a.interior[p] : 1;
+    const uint32_t p = p0 + 32u * j;
+    inter[j] = p < L32 ? a.interior[p] : 1;
   }
   uint32_t be[kRI], bs[kRI];
   uint32_t ce = 0, cs = 0;
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const bool in = striped_pos(j) < win.L;
+    const bool in = p0 + 32u * j < L32;
     be[j] = __ballot_sync(0xffffffffu, in && exc_word<DIST>(*P, wds[j]));
     bs[j] = __ballot_sync(0xffffffffu, inter[j] == 0);
     ce += __popc(be[j]);
@@ -361,49 +378,56 @@ __global__ void __launch_bounds__(kRT, ZF_EMIT_MINB)
   }
   uint32_t eidx, rank;
   warp_base2(ce, cs, wb, &eidx, &rank);
-  eidx += a.boff_exc[(uint64_t)blockIdx.x * a.boff_stride];
-  rank += a.boff_start[blockIdx.x];
+  eidx += boff_e;
+  rank += boff_s;
+  const uint32_t n32 = (uint32_t)a.n;  // n < 2^31
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
     const bool is_ex = (be[j] >> lane) & 1, is_st = (bs[j] >> lane) & 1;
     const uint32_t e_i = eidx + __popc(be[j] & lt), r_i = rank + __popc(bs[j] & lt);
-    if (is_st && r_i < a.n) {
-      const uint64_t p = striped_pos(j);
+    if (is_st && r_i < n32) {
+      const uint32_t p = p0 + 32u * j;
       double v;
-      uint32_t nw = 1, meta;
+      uint32_t nw = 1;
       if (is_ex) {
         nw = a.len[e_i];
         v = a.val[e_i];
-        meta = a.meta[e_i];
-        if (a.counters)
-          for (int q = 0; q < 6; ++q) c[q] += a.cnt[(uint64_t)e_i * 6 + q];
       } else {
         v = __dmul_rn(kSigned<DIST> ? __ll2double_rn((long long)wds[j])
                                     : __ull2double_rn(wds[j]),
                       __ldg(sx + (wds[j] & 0xFF) + 1));
-        meta = ((uint32_t)wds[j] & 0xFF) | (ZF_PATH_FAST << 8);
-        c[0] += 1;
-        c[1] += 1;
       }
       if (nw != kIncomplete) {
         out[r_i] = to_out<OutT>(v);
-        if (a.recs) {
-          zf_path_rec r;
-          r.start = p;
-          r.nwords = nw;
-          r.layer = (uint8_t)(meta & 0xFF);
-          r.path = (uint8_t)((meta >> 8) & 0xFF);
-          r.attempts = (uint16_t)(meta >> 16);
-          a.recs[r_i] = r;
+        if constexpr (FULL) {
+          uint32_t meta;
+          if (is_ex) {
+            meta = a.meta[e_i];
+            if (a.counters)
+              for (int q = 0; q < 6; ++q) c[q] += a.cnt[(uint64_t)e_i * 6 + q];
+          } else {
+            meta = ((uint32_t)wds[j] & 0xFF) | (ZF_PATH_FAST << 8);
+            c[0] += 1;
+            c[1] += 1;
+          }
+          if (a.recs) {
+            zf_path_rec r;
+            r.start = p;
+            r.nwords = nw;
+            r.layer = (uint8_t)(meta & 0xFF);
+            r.path = (uint8_t)((meta >> 8) & 0xFF);
+            r.attempts = (uint16_t)(meta >> 16);
+            a.recs[r_i] = r;
+          }
         }
-        if (r_i + 1 == a.n) *a.consumed = p + nw;
+        if (r_i + 1 == n32) *a.consumed = (unsigned long long)p + nw + 1;  // 0: not reached
       }
     }
     eidx += __popc(be[j]);
     rank += __popc(bs[j]);
   }
-  if (a.counters) {  // counted fills only: 6 atomics per warp on 6 addresses
+  if (FULL && a.counters) {  // counted fills only: 6 atomics per warp on 6 addresses
     for (int q = 0; q < 6; ++q) {
       unsigned long long v = c[q];
       for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -589,25 +613,48 @@ __global__ void __launch_bounds__(128)
   const uint64_t warp_first = t - lane;
   const uint64_t p0 = t * kXoBlock;
   const uint32_t lmax = (uint32_t)__ldg(&P->lmax);  // hoisted: one load per thread
+  uint32_t* const my_slots = slots + t * kClsCap;
   uint32_t k = 0;
-  for (int c = 0; c < kXoBlock; c += 32) {
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-      const uint64_t w = g.next();
-      tile[wid][lane][j] = w;
-      const uint64_t p = p0 + c + j;
-      const bool exc = kTrad<DIST> ? exc_word<DIST>(*P, w) : ((uint32_t)w & 0xFFu) >= lmax;
-      if (exc && p < n) {
-        if (k < kClsCap) slots[t * kClsCap + k] = (uint32_t)p;
-        ++k;
+  auto exc_of = [&](uint64_t w) -> bool {
+    return kTrad<DIST> ? exc_word<DIST>(*P, w) : ((uint32_t)w & 0xFFu) >= lmax;
+  };
+  if ((warp_first + 32) * kXoBlock <= n) {
+    // the whole warp's segments lie inside the window (every warp but the
+    // last): no per-word bounds, the slot store predicated (an overflowing
+    // segment keeps writing its last slot; the flag below reports it)
+    for (int c = 0; c < kXoBlock; c += 32) {
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const uint64_t w = g.next();
+        tile[wid][lane][j] = w;
+        if (exc_of(w)) my_slots[min(k, (uint32_t)kClsCap - 1)] = (uint32_t)(p0 + c + j);
+        k += exc_of(w);
       }
+      __syncwarp();
+      uint64_t* o = out + warp_first * kXoBlock + c + lane;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) o[(uint64_t)r * kXoBlock] = tile[wid][r][lane];
+      __syncwarp();
     }
-    __syncwarp();
-    for (int r = 0; r < 32; ++r) {
-      const uint64_t idx = (warp_first + r) * kXoBlock + c + lane;
-      if (idx < n) out[idx] = tile[wid][r][lane];
+  } else {
+    for (int c = 0; c < kXoBlock; c += 32) {
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const uint64_t w = g.next();
+        tile[wid][lane][j] = w;
+        const uint64_t p = p0 + c + j;
+        if (exc_of(w) && p < n) {
+          if (k < kClsCap) my_slots[k] = (uint32_t)p;
+          ++k;
+        }
+      }
+      __syncwarp();
+      for (int r = 0; r < 32; ++r) {
+        const uint64_t idx = (warp_first + r) * kXoBlock + c + lane;
+        if (idx < n) out[idx] = tile[wid][r][lane];
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (p0 < n) {
     slot_cnt[t] = k < kClsCap ? k : kClsCap;
@@ -617,10 +664,24 @@ __global__ void __launch_bounds__(128)
 
 __global__ void cls_compact(const uint32_t* __restrict__ slot_cnt, const uint32_t* __restrict__ coff,
                             uint64_t T, const uint32_t* __restrict__ slots,
-                            uint32_t* __restrict__ E) {
+                            uint32_t* __restrict__ E, uint32_t cap) {
   const uint64_t slot = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t t = slot / kClsCap, k = slot % kClsCap;
-  if (t < T && k < slot_cnt[t]) E[coff[t] + k] = slots[slot];
+  if (t < T && k < slot_cnt[t] && coff[t] + k < cap) E[coff[t] + k] = slots[slot];
+}
+
+// m above the bound the host sized the exceptional arrays for: clamp it (the
+// window is redone with exact sizes) and flag it
+__global__ void clamp_m(uint32_t* __restrict__ pm, uint32_t cap, unsigned int* __restrict__ flags) {
+  if (*pm > cap) {
+    *pm = cap;
+    atomicOr(flags, 2u);
+  }
+}
+
+// the segment-slot overflow of words_cls as a flag of this window
+__global__ void copy_flag(const unsigned int* __restrict__ src, unsigned int* __restrict__ flags) {
+  if (*src) atomicOr(flags, 1u);
 }
 
 // pre-classified window (words_cls): slots per segment + overflow flag
@@ -685,20 +746,90 @@ int device_scan(Workspace& ws, const T* in, T* out, uint64_t n, Op op, T init, T
   return cuda_status(cudaGetLastError());
 }
 
+// One window.  Normally no host synchronisation until the end: the exceptional
+// arrays are sized for a bound on their count m (random streams have ~1.6 % of
+// positions exceptional, the bound is 6.25 % + 4096) and every kernel reads m
+// from the device.  A window whose m exceeds the bound, or whose generator
+// segments overflowed their slots, is flagged and redone with exact sizes
+// (`exact`: one synchronisation to read m).
+// Exclusive scan of a short array (<= kSmallScan entries) by one 1024-thread
+// block: one launch where CUB takes two plus a total kernel.  Fused extras:
+// STARTS -- the input is the per-block interior count and the scanned value
+// is the block's start count (block length - interior words); the total is
+// written to *total, and if cap != 0 clamped to cap with flag bit 2.
+constexpr uint32_t kSmallScan = 1u << 13;  // one SM: longer arrays go to CUB
+template <typename T, class Op, bool STARTS>
+__global__ void __launch_bounds__(1024)
+    scan_small(const T* __restrict__ in, T* __restrict__ out, uint32_t n, T init, Op op,
+               T* __restrict__ total, uint32_t cap, unsigned int* __restrict__ flags, uint64_t L) {
+  __shared__ T wb[32];
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t b = threadIdx.x * per, e = min(n, b + per);
+  auto val = [&](uint32_t i) -> T {
+    if constexpr (STARTS) {
+      const uint64_t len = std::min<uint64_t>(L, (uint64_t)(i + 1) * kRB) - (uint64_t)i * kRB;
+      return (T)(len - in[i]);
+    } else {
+      return in[i];
+    }
+  };
+  T loc = init;
+  for (uint32_t i = b; i < e; ++i) loc = op(loc, val(i));
+  T tot;
+  T run = op(init, block_exclusive<T>(loc, init, op, wb, &tot));
+  for (uint32_t i = b; i < e; ++i) {
+    const T v = val(i);
+    out[i] = run;
+    run = op(run, v);
+  }
+  if (threadIdx.x == 0 && total) {
+    T t = op(init, tot);
+    if (cap && t > (T)cap) {
+      t = (T)cap;
+      atomicOr(flags, 2u);
+    }
+    *total = t;
+  }
+}
+
+// exclusive scan of n entries, reduction into *total (nullable); cap != 0
+// clamps the total (flag bit 2), STARTS as in scan_small
+template <typename T, class Op, bool STARTS = false>
+int scan_n(Workspace& ws, const T* in, T* out, uint64_t n, Op op, T init, T* total,
+           cudaStream_t s, uint32_t cap = 0, unsigned int* flags = nullptr, uint64_t L = 0,
+           T* tmp_in = nullptr) {
+  if (n == 0) return ZF_OK;
+  if (n <= kSmallScan) {
+    scan_small<T, Op, STARTS><<<1, 1024, 0, s>>>(in, out, (uint32_t)n, init, op, total, cap,
+                                                  flags, L);
+    return cuda_status(cudaGetLastError());
+  }
+  const T* src = in;
+  if constexpr (STARTS) {  // large windows: the start counts first, then CUB
+    rp_block_starts<<<(uint32_t)((n + 255) / 256), 256, 0, s>>>(in, (uint32_t)n, L, tmp_in);
+    src = tmp_in;
+  }
+  ZF_TRY_STATUS(device_scan<T>(ws, src, out, n, op, init, total, s));
+  if (cap) clamp_m<<<1, 1, 0, s>>>(reinterpret_cast<uint32_t*>(total), cap, flags);
+  return cuda_status(cudaGetLastError());
+}
+
 template <int DIST, typename OutT>
 int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, zf_path_rec* recs,
                   int64_t* counters, uint64_t* consumed_host, bool* retry, cudaStream_t s,
-                  const PreClass* pre = nullptr) {
+                  const PreClass* pre = nullptr, bool exact = false) {
   *retry = false;
-  if (debug_on()) fprintf(stderr, "[zf] replay_window L=%llu nwords=%llu cursor=%llu n=%llu\n",
+  if (debug_on()) fprintf(stderr, "[zf] replay_window L=%llu nwords=%llu cursor=%llu n=%llu%s\n",
                           (unsigned long long)win.L, (unsigned long long)win.nwords,
-                          (unsigned long long)win.cursor, (unsigned long long)n);
+                          (unsigned long long)win.cursor, (unsigned long long)n,
+                          exact ? " (exact)" : "");
   const DevPack* dP = primary_pack<DIST>(t->dev);  // device address
   const uint64_t L = win.L;
   const uint32_t nb = (uint32_t)((L + kRB - 1) / kRB);
   Workspace ws(s);
   uint32_t *bcnt, *boff, *E, *bcnt2, *boff2;
-  unsigned long long* scal;  // [0] exc total, [1] start total, [2] consumed, [3..8] counters
+  // [0] exceptional count m (u32), [1] flags (u32) | [2] consumed, [3..8] counters
+  unsigned long long* scal;
   uint8_t* interior;
   ZF_TRY(ws.alloc(&bcnt, nb));
   ZF_TRY(ws.alloc(&boff, nb));
@@ -706,91 +837,97 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   ZF_TRY(ws.alloc(&boff2, nb));
   ZF_TRY(ws.alloc(&scal, 16));
   ZF_TRY(ws.alloc(&interior, L));
-  if (debug_on()) fprintf(stderr, "[zf] workspace allocated\n");
+  uint32_t* dm = reinterpret_cast<uint32_t*>(scal);
+  unsigned int* dflags = reinterpret_cast<unsigned int*>(scal) + 1;
   ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
-  ZF_TRY(cudaMemsetAsync(scal + 2, 0xFF, sizeof(unsigned long long), s));
   // exceptional positions: from the generator's slots, or two passes here
   uint32_t* coff = nullptr;
-  uint32_t boff_stride = 1;
-  uint32_t m = 0;
-  bool use_pre = pre != nullptr;
+  const bool use_pre = pre != nullptr && !exact;
+  const uint32_t boff_stride = use_pre ? (uint32_t)(kRB / kXoBlock) : 1u;
+  // the bound the exceptional arrays are sized for (exact: m itself)
+  uint32_t cap = exact ? 0u : (uint32_t)std::min<uint64_t>(L, L / 16 + 4096);
   if (use_pre) {
     ZF_TRY(ws.alloc(&coff, pre->T));
-    ZF_TRY_STATUS(device_scan<uint32_t>(ws, pre->slot_cnt, coff, pre->T, Add(), 0u,
-                                        reinterpret_cast<uint32_t*>(scal), s));
-    unsigned int ovf = 0;
-    ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    ZF_TRY(cudaMemcpyAsync(&ovf, pre->overflow, sizeof ovf, cudaMemcpyDeviceToHost, s));
-    ZF_TRY(cudaStreamSynchronize(s));
-    if (ovf) use_pre = false;  // some segment overflowed its slots: classify here
-    else boff_stride = (uint32_t)(kRB / kXoBlock);
-  }
-  if (!use_pre) {
+    ZF_TRY_STATUS(scan_n<uint32_t>(ws, pre->slot_cnt, coff, pre->T, Add(), 0u, dm, s, cap, dflags));
+    copy_flag<<<1, 1, 0, s>>>(pre->overflow, dflags);
+  } else {
     rp_count_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, bcnt);
     dbg("rp_count_exc", s);
-    ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt, boff, nb, Add(), 0u,
-                                        reinterpret_cast<uint32_t*>(scal), s));
+    ZF_TRY_STATUS(scan_n<uint32_t>(ws, bcnt, boff, nb, Add(), 0u, dm, s, cap, dflags));
     dbg("scan_exc", s);
-    ZF_TRY(cudaMemcpyAsync(&m, scal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  }
+  if (exact) {
+    ZF_TRY(cudaMemcpyAsync(&cap, dm, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     ZF_TRY(cudaStreamSynchronize(s));
   }
   ExcOut eo;
   uint8_t *head, *real;
   uint64_t *bmax, *bpre;
-  const uint32_t nbE = (m + kRB - 1) / kRB;
-  ZF_TRY(ws.alloc(&E, m));
-  ZF_TRY(ws.alloc(&eo.len, m));
-  ZF_TRY(ws.alloc(&eo.val, m));
-  ZF_TRY(ws.alloc(&eo.meta, m));
-  ZF_TRY(ws.alloc(&eo.cnt, (uint64_t)m * 6));
-  ZF_TRY(ws.alloc(&head, m));
-  ZF_TRY(ws.alloc(&real, m));
+  const uint32_t nbE = (cap + kRB - 1) / kRB;
+  ZF_TRY(ws.alloc(&E, cap));
+  ZF_TRY(ws.alloc(&eo.len, cap));
+  ZF_TRY(ws.alloc(&eo.val, cap));
+  ZF_TRY(ws.alloc(&eo.meta, cap));
+  ZF_TRY(ws.alloc(&eo.cnt, (uint64_t)cap * 6));
+  ZF_TRY(ws.alloc(&head, cap));
+  ZF_TRY(ws.alloc(&real, cap));
   ZF_TRY(ws.alloc(&bmax, nbE));
   ZF_TRY(ws.alloc(&bpre, nbE));
   if (use_pre) {
     const uint64_t slots = pre->T * kClsCap;
     cls_compact<<<(uint32_t)((slots + 255) / 256), 256, 0, s>>>(pre->slot_cnt, coff, pre->T,
-                                                                pre->slots, E);
+                                                                pre->slots, E, cap);
   } else {
-    rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E);
+    rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E, cap);
   }
   dbg("compact", s);
-  if (m) {
+  if (cap) {
     constexpr int kPacks = kPacksOf<DIST>;
     const size_t smem = kPacks * sizeof(DevPack);
     ZF_TRY(cudaFuncSetAttribute(rp_draw_exc<DIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-    rp_draw_exc<DIST><<<(m + kRT - 1) / kRT, kRT, smem, s>>>(t->dev, win, E, m, eo);
-  dbg("rp_draw_exc<DIST>", s);
-    rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, m, bmax);
-  dbg("rp_reach_max", s);
-    ZF_TRY_STATUS(device_scan<uint64_t>(ws, bmax, bpre, nbE, Max(), 0ull, nullptr, s));
-    rp_heads<<<nbE, kRT, 0, s>>>(E, eo.len, m, bpre, head);
-  dbg("rp_heads", s);
-    ZF_TRY(cudaMemsetAsync(real, 0, m, s));
-    const uint64_t walkers = (m + kWalkChunk - 1) / kWalkChunk;
-    rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, m, real);
-  dbg("rp_walk", s);
+    rp_draw_exc<DIST><<<(cap + kRT - 1) / kRT, kRT, smem, s>>>(t->dev, win, E, dm, eo);
+    dbg("rp_draw_exc<DIST>", s);
+    rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, dm, bmax);
+    dbg("rp_reach_max", s);
+    ZF_TRY_STATUS(scan_n<uint64_t>(ws, bmax, bpre, nbE, Max(), 0ull, nullptr, s));
+    rp_heads<<<nbE, kRT, 0, s>>>(E, eo.len, dm, bpre, head);
+    dbg("rp_heads", s);
+    // (rp_walk writes real[i] for every i < m: entry 0 is always a head)
+    const uint64_t walkers = (cap + kWalkChunk - 1) / kWalkChunk;
+    rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, dm, real);
+    dbg("rp_walk", s);
   }
   ZF_TRY(cudaMemsetAsync(interior, 0, L, s));
   ZF_TRY(cudaMemsetAsync(bcnt, 0, nb * sizeof(uint32_t), s));  // reused: interior per block
-  if (m) rp_mark<<<(m + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, m, L, interior, bcnt);
+  if (cap) rp_mark<<<(cap + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, dm, L, interior, bcnt);
   dbg("rp_mark", s);
-  rp_block_starts<<<(nb + 255) / 256, 256, 0, s>>>(bcnt, nb, L, bcnt2);
-  dbg("rp_block_starts", s);
-  ZF_TRY_STATUS(device_scan<uint32_t>(ws, bcnt2, boff2, nb, Add(), 0u, nullptr, s));
+  ZF_TRY_STATUS((scan_n<uint32_t, Add, true>(ws, bcnt, boff2, nb, Add(), 0u, nullptr, s, 0,
+                                             nullptr, L, bcnt2)));
+  dbg("block starts", s);
   EmitArgs a{interior, use_pre ? coff : boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
              counters ? scal + 3 : nullptr, scal + 2, boff_stride};
-  rp_emit<DIST, OutT><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
-  dbg("OutT>", s);
+  if (recs || counters)
+    rp_emit<DIST, OutT, true><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
+  else
+    rp_emit<DIST, OutT, false><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
+  dbg("rp_emit", s);
   ZF_TRY(cudaGetLastError());
-  unsigned long long consumed = 0;
-  ZF_TRY(cudaMemcpyAsync(&consumed, scal + 2, sizeof consumed, cudaMemcpyDeviceToHost, s));
+  unsigned long long res[3] = {0, 0, 0};  // m | flags, consumed
+  ZF_TRY(cudaMemcpyAsync(res, scal, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   ZF_TRY(cudaStreamSynchronize(s));
-  if (consumed == ~0ull) {
+  if (res[0] >> 32) {
+    // a segment overflowed its slots or m exceeded the bound: the results of
+    // this pass are void (the output is rewritten)
+    if (exact) return ZF_ERANGE;  // (unreachable: exact passes set no flags)
+    return replay_window<DIST, OutT>(t, win, out, n, recs, counters, consumed_host, retry, s, pre,
+                                     true);
+  }
+  if (res[2] == 0) {  // the window holds fewer than n draws
     *retry = true;
     return ZF_OK;
   }
+  const unsigned long long consumed = res[2] - 1;
   if (counters) add_counters<<<1, 32, 0, s>>>(scal + 3, reinterpret_cast<unsigned long long*>(counters));
   *consumed_host = consumed;
   return cuda_status(cudaGetLastError());

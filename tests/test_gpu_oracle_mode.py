@@ -164,6 +164,26 @@ def test_adversarial_replay_all_exceptional(zf, orc, cuda):
         assert int(s.source.state[0]) == used
 
 
+@pytest.mark.parametrize("frac", [0.9, 0.07, 0.04])
+def test_replay_exceptional_count_above_the_bound(zf, orc, cuda, frac):
+    """The exceptional arrays are sized for a bound (6.25 % of the window +
+    4096) without a host round trip; windows with more exceptional words (90 %)
+    are redone with exact sizes, windows near the bound (7 %, 4 %) pass
+    either way.  Values and words consumed equal the reference's."""
+    rng = np.random.default_rng(int(frac * 100))
+    m = 400_000
+    words = rng.integers(0, 2**63, m, dtype=np.uint64) << np.uint64(8)
+    exc = rng.random(m) < frac
+    words[exc] |= np.uint64(0xFF)
+    words[~exc] |= rng.integers(0, 200, int((~exc).sum()), dtype=np.uint64)
+    for dist in DISTS:
+        s = cls_of(zf, dist)(source=zf.UniformSource.replay(words), device=cuda)
+        got = s.fill(100_000).cpu().numpy()
+        want, _, _, used = orc.fill_stream(dist, 100_000, replay_words=words)
+        assert np.array_equal(bits(got), bits(want)), dist
+        assert int(s.source.state[0]) == used
+
+
 def test_cycling_replay_is_an_error_not_a_hang(zf, cuda):
     """A short wrapping list on which a normal-tail draw can never finish (the
     reference would loop forever) fails with ZF_ERANGE instead of hanging."""
