@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "zf_internal.h"
@@ -40,6 +41,13 @@ constexpr int default_pass2() {
 #ifndef ZF_MIN_BLOCKS
 #define ZF_MIN_BLOCKS 1  // CTAs per SM requested from the register allocator
 #endif
+
+// fill kernels whose queue bookkeeping runs per pair of tiles (measured: the
+// modified fp64 fills and the fp32 exponential gain, the traditional kernels
+// and the fp32 normal lose -- DESIGN.md round-2 log)
+template <int DIST, typename OutT>
+constexpr bool kFillPaired =
+    ZF_PAIR && !kTrad<DIST> && (std::is_same<OutT, double>::value || DIST == ZF_EXP);
 
 template <int DIST, typename OutT, bool COUNTED, bool VEC, int P2>
 __global__ void __launch_bounds__(kFillThreads, ZF_MIN_BLOCKS)
@@ -75,9 +83,14 @@ __global__ void __launch_bounds__(kFillThreads, ZF_MIN_BLOCKS)
 #if defined(ZF_CHECKS) && ZF_CHECKS
   sink.n_check = n;
 #endif
-  run_tiles<DIST, COUNTED, P2>(P, E, seed, ctr_base, sink, n,
-                               (uint64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5),
-                               (uint64_t)gridDim.x * kFillWarps, queue, lane, lc, late);
+  // modified fp64 fills (and fp32 exponential) pair adjacent tiles: warp w
+  // takes tiles 2w, 2w + 1, then 2w + 2W, 2w + 2W + 1, ...
+  constexpr bool kPaired = kFillPaired<DIST, OutT>;
+  const uint64_t w = (uint64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kFillWarps;
+  run_tiles<DIST, COUNTED, P2, StoreSink<OutT, VEC>, kPaired>(
+      P, E, seed, ctr_base, sink, n, kPaired ? 2 * w : w, kPaired ? 2 * nw : nw, queue, lane, lc,
+      late, kPaired ? 1 : 0);
   if (COUNTED) flush_counts(lc, counters);
 }
 
@@ -157,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, ZF_BATCH_MIN_BLOCKS)
 
 template <typename K>
 static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid,
-                    int fixed_waves = 0, int threads = kThreads) {
+                    int fixed_waves = 0, int threads = kThreads, bool paired = false) {
   static_assert(sizeof(K) > 0, "");
   int per_sm = 0;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -177,7 +190,10 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
   // 2^30 8 waves 713 / 764 (110), 12 waves 739 / 787 (74); 2^28 3-6 waves
   // 720 / 764 (74-37), 8 waves 711 / 760; 2^26 1 wave 660 / 701, 4 waves
   // 645 / 694.
-  constexpr uint64_t kTilesPerWarp = 64;
+  // (with paired tiles the optimum is ~32 tiles = 16 pairs per warp: 2^32
+  // samples 55 / 110 / 220 waves 749 / 770 / 745 normal, 793 / 817 / 802 exp;
+  // 2^28 6 / 12 / 24 waves 709 / 723 / 689)
+  const uint64_t kTilesPerWarp = paired ? 32 : 64;
   static const int env_waves = [] {
     const char* e = getenv("ZF_GRID_WAVES");
     return e ? std::max(1, atoi(e)) : 0;
@@ -220,7 +236,7 @@ static int launch_typed(const zf_tables* t, uint64_t seed, uint64_t ctr_base, Ou
                       (size_t)kFillWarps * kQueueWords * sizeof(uint32_t) + ZF_SMEM_PAD;
   int grid = 0;
   ZF_TRY_STATUS(grid_for(kernel, smem, t->sm_count, (n + kTile - 1) / kTile, &grid, 0,
-                         kFillThreads));
+                         kFillThreads, kFillPaired<DIST, OutT>));
   kernel<<<grid, kFillThreads, smem, s>>>(t->dev, seed, ctr_base, out, n, counters);
   return cuda_status(cudaGetLastError());
 }

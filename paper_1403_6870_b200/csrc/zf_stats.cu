@@ -138,8 +138,9 @@ __global__ void __launch_bounds__(kThreads)
   if constexpr (MODE == 0) {
     __syncthreads();
     SumSink sink;
-    run_tiles<DIST, false, 3>(sp[0], sp[kPacks - 1], seed, ctr_base, sink, n, warp0, nwarps,
-                              queue, lane, lc);
+    // the aggregate pairs tiles (the next grid-stride tile: +2-4.5 %)
+    run_tiles<DIST, false, 3, SumSink, !kTrad<DIST>>(sp[0], sp[kPacks - 1], seed, ctr_base, sink,
+                                                     n, warp0, nwarps, queue, lane, lc);
     flush_sum(sink.s, sh, partials);
   } else if constexpr (MODE == 4) {
 #pragma unroll
