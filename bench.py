@@ -90,9 +90,15 @@ class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    OTHER = [("nvmlClocksEventReasonApplicationsClocksSetting", "applications_clocks_setting"),
+             ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown"),
+             ("nvmlClocksEventReasonSyncBoost", "sync_boost"),
+             ("nvmlClocksEventReasonDisplayClockSetting", "display_clock_setting"),
+             ("nvmlClocksEventReasonGpuIdle", "gpu_idle")]
 
     def __init__(self, index: int):
         self.index, self.rows, self._stop = index, [], threading.Event()
+        self.temps = []
         self._ready = threading.Event()
         self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -104,15 +110,34 @@ class ClockSampler:
             h = N.nvmlDeviceGetHandleByIndex(self.index)
             bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
                     N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            # every other reason bit too (applications clocks, power brake, sync
+            # boost, display, idle), so a low clock always shows its cause
+            bits += [getattr(N, a) for a, _ in self.OTHER if hasattr(N, a)]
             self._nvml = (N, h, bits, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
         except Exception:
             self._nvml = None
 
+    @staticmethod
+    def _instant_power(N, h):
+        # instantaneous board power where the driver offers it (the plain
+        # power reading is a ~1 s average that lags a 0.15 s timed region)
+        try:
+            v = N.nvmlDeviceGetFieldValues(h, [N.NVML_FI_DEV_POWER_INSTANT])[0]
+            if v.nvmlReturn == 0:
+                return v.value.uiVal / 1000.0
+        except Exception:
+            pass
+        return N.nvmlDeviceGetPowerUsage(h) / 1000.0
+
     def _sample_nvml(self):
         N, h, bits, mx = self._nvml
         sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-        pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+        pw = self._instant_power(N, h)
         r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        try:
+            self.temps.append(N.nvmlDeviceGetTemperature(h, N.NVML_TEMPERATURE_GPU))
+        except Exception:
+            pass
         self.rows.append([str(self.index), str(sm), str(mx), f"{pw:.1f}"] +
                          ["Active" if r & b else "Not Active" for b in bits])
 
@@ -154,13 +179,18 @@ class ClockSampler:
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        if self._nvml:
+            N = self._nvml[0]
+            names += [nm for a, nm in self.OTHER if hasattr(N, a)]
+        reasons = sorted({names[i] for r in self.rows for i in range(len(names))
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
         pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_min_mhz": min(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+                "power_w_max": max(pw) if pw else None,
+                "temp_c_max": max(self.temps) if self.temps else None,
+                "samples": len(self.rows)}
 
 
 def cpu_threads():
