@@ -63,7 +63,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=N_DEFAULT)
+    p.add_argument("--n-per-gpu", "--n", dest="n", type=int, default=N_DEFAULT)
     p.add_argument("--seed", type=int, default=SEED)
     p.add_argument("--cpu-seconds", type=float, default=10.0,
                    help="target duration of the CPU baseline sample")
@@ -353,10 +353,19 @@ def main():
     import paper_1403_6870_b200 as zf
     from paper_1403_6870_b200 import scale, shard
 
+    # ZF_BENCH_SHARE_DEVICE=1 (tests only, tests/test_gpu_bench_multirank.py):
+    # every rank on cuda:0 over gloo, to exercise the N > 1 code path on a
+    # one-GPU box -- its numbers are not a scaling measurement
+    share = os.environ.get("ZF_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     barrier = dist.barrier if world > 1 else None
     n = args.n
     stream = torch.cuda.current_stream(dev)
@@ -511,7 +520,7 @@ def main():
                          "bytes_per_sample": 8, "write_peak_gbs": wp,
                          "frac_of_write_peak": achieved / wp if wp else None,
                          "kernel": "fill_ctr_kernel<normal,f64>"},
-            "validation": {**c3, "allreduce": "nccl" if world > 1 else "none"},
+            "validation": {**c3, "allreduce": dist.get_backend() if world > 1 else "none"},
             "clocks": clk.summary(),
             "gpu_launches": args.steps,  # one fill_ctr_kernel launch per timed step
             "e2e": e2e,

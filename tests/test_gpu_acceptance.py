@@ -122,3 +122,45 @@ def test_per_box_acceptance_matches_slot_masses(zf, cuda):
                 assert sampler.overhang_attempt(j, float(ux[i]), float(uy[i]))[0] == bool(acc[i])
             worst = max(worst, abs(acc.mean() - p) / math.sqrt(p * (1.0 - p) / m))
     assert worst <= 3.0  # the reference's gate (criterion 5); 2.70 with this seed
+
+
+_DIGEST = r"""
+import hashlib, sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_1403_6870_b200 as zf
+dev = torch.device("cuda", 0)
+h = hashlib.sha256()
+for cls in (zf.ExpSampler, zf.NormalSampler):
+    h.update(cls(source=zf.UniformSource.counter(7, 1 << 40), device=dev)
+             .fill(3 * (1 << 20) + 11).cpu().numpy().tobytes())
+    h.update(cls(source=zf.UniformSource(42), device=dev).fill(100_003).cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_determinism_across_processes_and_grids(zf, cuda):
+    """The reference's criterion 7 (tests/test_acceptance.py:168-182): the same
+    seed gives the same stream in a fresh process.  Here also under other grid
+    shapes (ZF_GRID_WAVES), since production output depends only on (seed, K)."""
+    import hashlib
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    h = hashlib.sha256()
+    for cls in (zf.ExpSampler, zf.NormalSampler):
+        h.update(cls(source=zf.UniformSource.counter(7, 1 << 40), device=cuda)
+                 .fill(3 * (1 << 20) + 11).cpu().numpy().tobytes())
+        h.update(cls(source=zf.UniformSource(42), device=cuda).fill(100_003).cpu().numpy()
+                 .tobytes())
+    here = h.hexdigest()
+    for waves in (None, "1", "7"):
+        env = dict(os.environ)
+        if waves:
+            env["ZF_GRID_WAVES"] = waves
+        out = subprocess.run([sys.executable, "-c", _DIGEST.format(root=root)], env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert out.stdout.strip().splitlines()[-1] == here, waves
