@@ -294,21 +294,23 @@ __global__ void rp_walk(const uint32_t* __restrict__ E, const uint32_t* __restri
   }
 }
 
-// ---- D: interior marks -----------------------------------------------------------
-// mark the interior words of every real draw, and count them per emit block
-// (real draws never overlap, so the counts are exact)
+// ---- D: interior counts --------------------------------------------------------
+// count the interior words of every real draw per emit block (real draws never
+// overlap, so the counts are exact) and record, for every block a draw enters
+// from an earlier block, how many of its leading positions it covers (`spill`;
+// the emit kernel marks the rest of its block's interior words itself)
 __global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
                         const uint8_t* __restrict__ real, const uint32_t* __restrict__ pm,
-                        uint64_t L, uint8_t* __restrict__ interior,
-                        uint32_t* __restrict__ block_int) {
+                        uint64_t L, uint32_t* __restrict__ block_int,
+                        uint32_t* __restrict__ spill) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *pm || !real[i]) return;
   const uint64_t p = E[i];
   const uint64_t stop = len[i] == kIncomplete ? L : std::min<uint64_t>(p + len[i], L);
-  for (uint64_t q = p + 1; q < stop; ++q) interior[q] = 1;
   for (uint64_t q = p + 1; q < stop;) {
     const uint64_t b = q / kRB, e = std::min<uint64_t>(stop, (b + 1) * kRB);
     atomicAdd(block_int + b, (uint32_t)(e - q));
+    if (q == b * kRB) spill[b] = (uint32_t)(e - q);  // entered from an earlier block
     q = e;
   }
 }
@@ -325,7 +327,11 @@ __global__ void rp_block_starts(const uint32_t* __restrict__ block_int, uint32_t
 
 // ---- E: emit -------------------------------------------------------------------------
 struct EmitArgs {
-  const uint8_t* interior;
+  const uint32_t* E;             // exceptional positions (sorted)
+  const uint8_t* real;           // real[i]: E[i] starts a draw
+  const uint32_t* pm;            // m (device)
+  const uint32_t* spill;         // leading positions of a block covered by an earlier draw
+  uint32_t nseg;                 // boff_exc entries (segments or blocks)
   const uint32_t* boff_exc;
   const uint32_t* boff_start;
   const uint32_t* len;
@@ -358,13 +364,48 @@ __global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
   // the block's offsets do not depend on the words: in flight with them
   const uint32_t boff_e = __ldg(a.boff_exc + (uint64_t)blockIdx.x * a.boff_stride);
   const uint32_t boff_s = __ldg(a.boff_start + blockIdx.x);
+  const uint64_t nxt = (uint64_t)(blockIdx.x + 1) * a.boff_stride;
+  // (m may be clamped to the bound the arrays were sized for: that pass is
+  // flagged and redone, so entries past it are only ever skipped here)
+  const uint32_t m = __ldg(a.pm);
+  const uint32_t e_end = min(nxt < a.nseg ? __ldg(a.boff_exc + nxt) : m, m);
+  const uint32_t spill = __ldg(a.spill + blockIdx.x);
+  // this thread's first entry of the block's slice, in flight with the words
+  const uint32_t i0 = boff_e + threadIdx.x;
+  const bool has0 = i0 < e_end;
+  const uint8_t real0 = has0 ? __ldg(a.real + i0) : 0;
+  const uint32_t p_0 = has0 ? __ldg(a.E + i0) : 0, l_0 = has0 ? __ldg(a.len + i0) : 0;
   uint64_t wds[kRI];
-  uint8_t inter[kRI];
   load_striped(win, wds);
+  // interior words of this block as a 2048-bit map: the real draws that start
+  // in it (its slice of E) and the one an earlier block's draw spills in
+  __shared__ uint32_t imap[kRB / 32];
+  const uint32_t b0 = blockIdx.x * (uint32_t)kRB;
+  if (threadIdx.x < kRB / 32) {
+    const uint32_t lo = threadIdx.x * 32u;  // word w covers positions b0 + [32w, 32w + 32)
+    imap[threadIdx.x] = spill >= lo + 32u ? 0xFFFFFFFFu : spill > lo ? (1u << (spill - lo)) - 1u : 0u;
+  }
+  __syncthreads();
+  for (uint32_t i = i0; i < e_end; i += kRT) {
+    const bool first = i == i0;
+    if (!(first ? real0 : __ldg(a.real + i))) continue;
+    const uint32_t p = first ? p_0 : __ldg(a.E + i), l = first ? l_0 : __ldg(a.len + i);
+    const uint32_t stop = l == kIncomplete ? L32 : min(p + l, L32);
+    for (uint32_t q = p + 1 - b0, qe = min(stop - b0, (uint32_t)kRB); q < qe;) {
+      // the run [q, qe) word by word
+      const uint32_t w = q >> 5, hi = min(qe, (w + 1) * 32u);
+      const uint32_t bits = (hi - q == 32 ? 0xFFFFFFFFu : ((1u << (hi - q)) - 1u)) << (q & 31);
+      atomicOr(&imap[w], bits);
+      q = hi;
+    }
+  }
+  __syncthreads();
+  uint8_t inter[kRI];
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
     const uint32_t p = p0 + 32u * j;
-    inter[j] = p < L32 ? a.interior[p] : 1;
+    const uint32_t r = p - b0;
+    inter[j] = p < L32 ? (uint8_t)((imap[r >> 5] >> (r & 31)) & 1u) : 1;
   }
   uint32_t be[kRI], bs[kRI];
   uint32_t ce = 0, cs = 0;
@@ -386,7 +427,7 @@ __global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
   for (int j = 0; j < kRI; ++j) {
     const bool is_ex = (be[j] >> lane) & 1, is_st = (bs[j] >> lane) & 1;
     const uint32_t e_i = eidx + __popc(be[j] & lt), r_i = rank + __popc(bs[j] & lt);
-    if (is_st && r_i < n32) {
+    if (is_st && r_i < n32 && !(is_ex && e_i >= m)) {
       const uint32_t p = p0 + 32u * j;
       double v;
       uint32_t nw = 1;
@@ -827,16 +868,15 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
   const uint64_t L = win.L;
   const uint32_t nb = (uint32_t)((L + kRB - 1) / kRB);
   Workspace ws(s);
-  uint32_t *bcnt, *boff, *E, *bcnt2, *boff2;
+  uint32_t *bcnt, *boff, *E, *bcnt2, *boff2, *spill;
   // [0] exceptional count m (u32), [1] flags (u32) | [2] consumed, [3..8] counters
   unsigned long long* scal;
-  uint8_t* interior;
   ZF_TRY(ws.alloc(&bcnt, nb));
+  ZF_TRY(ws.alloc(&spill, nb));
   ZF_TRY(ws.alloc(&boff, nb));
   ZF_TRY(ws.alloc(&bcnt2, nb));
   ZF_TRY(ws.alloc(&boff2, nb));
   ZF_TRY(ws.alloc(&scal, 16));
-  ZF_TRY(ws.alloc(&interior, L));
   uint32_t* dm = reinterpret_cast<uint32_t*>(scal);
   unsigned int* dflags = reinterpret_cast<unsigned int*>(scal) + 1;
   ZF_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(unsigned long long), s));
@@ -898,15 +938,16 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
     rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, dm, real);
     dbg("rp_walk", s);
   }
-  ZF_TRY(cudaMemsetAsync(interior, 0, L, s));
   ZF_TRY(cudaMemsetAsync(bcnt, 0, nb * sizeof(uint32_t), s));  // reused: interior per block
-  if (cap) rp_mark<<<(cap + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, dm, L, interior, bcnt);
+  ZF_TRY(cudaMemsetAsync(spill, 0, nb * sizeof(uint32_t), s));
+  if (cap) rp_mark<<<(cap + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, dm, L, bcnt, spill);
   dbg("rp_mark", s);
   ZF_TRY_STATUS((scan_n<uint32_t, Add, true>(ws, bcnt, boff2, nb, Add(), 0u, nullptr, s, 0,
                                              nullptr, L, bcnt2)));
   dbg("block starts", s);
-  EmitArgs a{interior, use_pre ? coff : boff, boff2, eo.len, eo.val, eo.meta, eo.cnt, n, recs,
-             counters ? scal + 3 : nullptr, scal + 2, boff_stride};
+  EmitArgs a{E, real, dm, spill, use_pre ? (uint32_t)pre->T : nb, use_pre ? coff : boff, boff2,
+             eo.len, eo.val, eo.meta, eo.cnt, n, recs, counters ? scal + 3 : nullptr, scal + 2,
+             boff_stride};
   if (recs || counters)
     rp_emit<DIST, OutT, true><<<nb, kRT, 0, s>>>(t->dev, win, a, static_cast<OutT*>(out));
   else
