@@ -505,6 +505,10 @@ __device__ __forceinline__ void xo_step(uint64_t s[4]) {
 #ifndef ZF_XO_BLOCK
 #define ZF_XO_BLOCK 1024
 #endif
+// block parents for the device xoshiro jump (xo_jump_block)
+#ifndef ZF_XO_PARENT
+#define ZF_XO_PARENT 1
+#endif
 constexpr int kXoBlock = ZF_XO_BLOCK;  // words per thread
 constexpr int kXoBits = 8;      // jump-table radix 256: <= 3 polynomials for 2^24 threads
 constexpr int kXoRadix = 1 << kXoBits;
@@ -573,12 +577,37 @@ __device__ __forceinline__ void xo_apply(const unsigned long long* __restrict__ 
 
 // start state of thread t's block: s0 jumped by t * kXoBlock words
 __device__ __forceinline__ void xo_jump_to(const uint64_t* __restrict__ table, uint64_t t,
-                                           uint64_t s[4]) {
+                                           uint64_t s[4], int first_level = 0) {
   const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(table);
-  for (int r = 0; r < kXoLevels && (t >> (kXoBits * r)) != 0; ++r) {
+  for (int r = first_level; r < kXoLevels && (t >> (kXoBits * r)) != 0; ++r) {
     const int d = (int)((t >> (kXoBits * r)) & (kXoRadix - 1));
     if (d) xo_apply(pp + ((size_t)r * (kXoRadix - 1) + d - 1) * 4, s);
   }
+}
+
+// The same for every thread of a block of consecutive t (blockDim.x divides
+// 256): thread 0 jumps to the block's parent (t with its base-256 digit 0
+// cleared, all higher digits) and shares it; every thread then applies only its
+// own digit 0 -- one polynomial application per thread instead of one per
+// nonzero digit (2-3 for windows of 2^26 words).  Includes a __syncthreads.
+__device__ __forceinline__ void xo_jump_block(const uint64_t* __restrict__ table, uint64_t t,
+                                              ulonglong4 s0, uint64_t s[4]) {
+  __shared__ uint64_t parent[4];
+  if (threadIdx.x == 0) {
+    uint64_t p[4] = {s0.x, s0.y, s0.z, s0.w};
+    xo_jump_to(table, t & ~(uint64_t)(kXoRadix - 1), p, 1);
+    parent[0] = p[0];
+    parent[1] = p[1];
+    parent[2] = p[2];
+    parent[3] = p[3];
+  }
+  __syncthreads();
+  s[0] = parent[0];
+  s[1] = parent[1];
+  s[2] = parent[2];
+  s[3] = parent[3];
+  const int d = (int)(t & (kXoRadix - 1));
+  if (d) xo_apply(reinterpret_cast<const unsigned long long*>(table) + (size_t)(d - 1) * 4, s);
 }
 
 // thread t owns words [t*B, (t+1)*B): start state = T^(t*B) s0, one jump
@@ -592,7 +621,11 @@ __global__ void __launch_bounds__(128)
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
+#if ZF_XO_PARENT
+  xo_jump_block(polys, t, s0, s);
+#else
   xo_jump_to(polys, t, s);
+#endif
   const uint64_t warp_first = t - lane;  // thread index of lane 0
   for (int c = 0; c < B; c += 32) {
 #pragma unroll 4
@@ -646,8 +679,12 @@ __global__ void __launch_bounds__(128)
   using G = typename std::conditional<GID == ZF_GEN_XOSHIRO256PP, XoGen, SmGen>::type;
   G g;
   if constexpr (GID == ZF_GEN_XOSHIRO256PP) {
+#if ZF_XO_PARENT
+    xo_jump_block(polys, t, s0, g.s);
+#else
     g = XoGen{{s0.x, s0.y, s0.z, s0.w}};
     xo_jump_to(polys, t, g.s);
+#endif
   } else {
     g = SmGen{s0.x + t * (uint64_t)kXoBlock * kGamma};
   }
