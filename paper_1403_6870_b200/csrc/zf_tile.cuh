@@ -82,6 +82,12 @@ constexpr int kQueueWords = kQueueCap + (ZF_COOP ? 128 : 0);
 #ifndef ZF_PAIR
 #define ZF_PAIR 1
 #endif
+// paired normal kernels: the second queue entry of a lane by a predicated
+// store as well (with 32 samples per lane mask, 83 % of pairs have a lane
+// holding two: 770 -> 775 G/s at 2^32)
+#ifndef ZF_SECOND_STORE
+#define ZF_SECOND_STORE 1
+#endif
 static_assert(kPerLane == 16 || !ZF_PAIR, "paired tiles need 16-bit lane masks");
 
 // ZF_CHECKS=1 (debug builds, tests/test_gpu_checked.py): device-side bounds and
@@ -666,11 +672,12 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                      ::"r"(qs + 4u * (uint32_t)slot), "r"(tag | (uint32_t)hb), "r"(mask)
                      : "memory");
         if (multi) {
-          if constexpr (DIST == ZF_EXP) {
+          if constexpr (DIST == ZF_EXP || (ZF_SECOND_STORE && PAIR)) {
           // exponential (1.56 % exceptional: a lane holds two in ~57 % of
-          // tiles): the second entry is predicated as well and the loop runs
-          // only for lanes with three or more.  (The normal kernel loses 6 %
-          // with it: +4 registers and a worse layout.)
+          // tiles) and paired normal kernels: the second entry is predicated
+          // as well and the loop runs only for lanes with three or more.
+          // (The unpaired normal kernel loses 6 % with it: +4 registers and
+          // a worse layout.)
           const uint32_t m2 = drop_top(mask);
           const int hb2 = 31 - __clz(m2);
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
