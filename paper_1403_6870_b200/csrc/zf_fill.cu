@@ -45,6 +45,11 @@ constexpr int default_pass2() {
 // fill kernels whose queue bookkeeping runs per pair of tiles (measured: the
 // modified fp64 fills and the fp32 exponential gain, the traditional kernels
 // and the fp32 normal lose -- DESIGN.md round-2 log)
+#ifndef ZF_FILL_NT
+// tiles per queue bookkeeping in the paired fill kernels (4: 64-bit lane masks
+// and four inlined pass-1 bodies -- 612 vs 772 G/s, measured and dropped)
+#define ZF_FILL_NT 2
+#endif
 template <int DIST, typename OutT>
 constexpr bool kFillPaired =
     ZF_PAIR && !kTrad<DIST> && (std::is_same<OutT, double>::value || DIST == ZF_EXP);
@@ -85,12 +90,12 @@ __global__ void __launch_bounds__(kFillThreads, ZF_MIN_BLOCKS)
 #endif
   // modified fp64 fills (and fp32 exponential) pair adjacent tiles: warp w
   // takes tiles 2w, 2w + 1, then 2w + 2W, 2w + 2W + 1, ...
-  constexpr bool kPaired = kFillPaired<DIST, OutT>;
+  constexpr int kNT = kFillPaired<DIST, OutT> ? ZF_FILL_NT : 1;  // adjacent tiles per warp step
   const uint64_t w = (uint64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5);
   const uint64_t nw = (uint64_t)gridDim.x * kFillWarps;
-  run_tiles<DIST, COUNTED, P2, StoreSink<OutT, VEC>, kPaired>(
-      P, E, seed, ctr_base, sink, n, kPaired ? 2 * w : w, kPaired ? 2 * nw : nw, queue, lane, lc,
-      late, kPaired ? 1 : 0);
+  run_tiles<DIST, COUNTED, P2, StoreSink<OutT, VEC>, kNT>(P, E, seed, ctr_base, sink, n, kNT * w,
+                                                         kNT * nw, queue, lane, lc, late,
+                                                         kNT > 1 ? 1 : 0);
   if (COUNTED) flush_counts(lc, counters);
 }
 

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     SumSink sink;
     // the aggregate pairs tiles (the next grid-stride tile: +2-4.5 %)
-    run_tiles<DIST, false, 3, SumSink, !kTrad<DIST>>(sp[0], sp[kPacks - 1], seed, ctr_base, sink,
+    run_tiles<DIST, false, 3, SumSink, kTrad<DIST> ? 1 : 2>(sp[0], sp[kPacks - 1], seed, ctr_base, sink,
                                                      n, warp0, nwarps, queue, lane, lc);
     flush_sum(sink.s, sh, partials);
   } else if constexpr (MODE == 4) {

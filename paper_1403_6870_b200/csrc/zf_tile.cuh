@@ -16,6 +16,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "zf_device.cuh"
 
 namespace zf {
@@ -554,6 +556,15 @@ __device__ __forceinline__ int warp_excl_mask(uint32_t mask, int lane, int* tota
   *total = __popc(any);
   return __popc(any & ((1u << lane) - 1u));
 }
+__device__ __forceinline__ int warp_excl_mask(uint64_t mask, int lane, int* total,
+                                              bool* multi_any = nullptr) {
+  const uint32_t multi = __ballot_sync(0xffffffffu, (mask & (mask - 1u)) != 0u);
+  if (multi_any) *multi_any = multi != 0u;
+  if (multi) return warp_excl_count(__popcll(mask), lane, total);
+  const uint32_t any = __ballot_sync(0xffffffffu, mask != 0u);
+  *total = __popc(any);
+  return __popc(any & ((1u << lane) - 1u));
+}
 
 // x without its highest set bit; 0 for x == 0 (the shift count is masked so
 // it stays defined when __clz(0) == 32)
@@ -578,7 +589,17 @@ __device__ __forceinline__ uint32_t mask_bit_offset(int b, int lane) {
 // bit-identical but slower on B200: their extra registers and code cost the
 // fast path more than they saved.)
 // A warp's whole share of a fill: tiles first_tile, first_tile + stride, ...
-template <int DIST, bool COUNTED, int P2, class Sink, bool PAIR_ = false>
+// lane-mask helpers for the 32-bit (one or two tiles) and 64-bit (four tiles)
+// masks of run_tiles
+__device__ __forceinline__ int mask_top(uint32_t m) { return 31 - __clz(m); }
+__device__ __forceinline__ int mask_top(uint64_t m) { return 63 - __clzll((long long)m); }
+__device__ __forceinline__ uint64_t drop_top(uint64_t x) {
+  return x & ~(0x8000000000000000ull >> (__clzll((long long)x) & 63));
+}
+__device__ __forceinline__ int mask_popc(uint32_t m) { return __popc(m); }
+__device__ __forceinline__ int mask_popc(uint64_t m) { return __popcll(m); }
+
+template <int DIST, bool COUNTED, int P2, class Sink, int NT_ = 1>
 __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, uint64_t seed,
                                           uint64_t ctr_base, Sink& sink, uint64_t n,
                                           uint64_t first_tile, uint64_t stride, uint32_t* q,
@@ -586,14 +607,18 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
                                           const uint64_t* late = nullptr,
                                           uint64_t pair_off = 0) {
   static_assert(P2 == 3 || P2 == 9, "unknown pass-2 policy");
-  constexpr bool PAIR = PAIR_ && ZF_PAIR;
-  constexpr int kEntBits = PAIR ? 5 : kPerLaneBits;  // mask-bit field of a queue entry
+  // tiles per queue bookkeeping (1, 2 or 4; ZF_PAIR=0 forces 1)
+  constexpr int NT = ZF_PAIR ? NT_ : 1;
+  static_assert(NT == 1 || NT == 2 || NT == 4, "1, 2 or 4 tiles per bookkeeping");
+  constexpr bool PAIR = NT > 1;
+  using Mask = typename std::conditional<NT == 4, uint64_t, uint32_t>::type;
+  constexpr int kEntBits = kPerLaneBits + (NT == 4 ? 2 : NT == 2 ? 1 : 0);  // mask-bit field
   // paired bookkeeping: the loop visits tiles first_tile + i * step, each with
   // its partner tile + off (pair_off = 0: the partner is the next grid-stride
   // tile, off = stride and step = 2 * stride; the fill kernel passes
   // adjacent pairs, off = 1 with a doubled first tile and stride)
   const uint64_t off = pair_off ? pair_off : stride;
-  const uint64_t step = (PAIR && !pair_off) ? 2 * stride : stride;
+  const uint64_t step = (PAIR && !pair_off) ? NT * stride : stride;
   // `late`: mbarrier (phase 0) of the table arrays only the rounds read
   bool tables_ready = late == nullptr;
   auto need_tables = [&]() {
@@ -617,9 +642,10 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
   };
   if constexpr (P2 == 9) {
     for (uint64_t tile = first_tile; tile < ntiles; tile += step) {
-      fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
-      if (PAIR && tile + off < ntiles)
-        fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, (tile + off) * kTile, lane, lc);
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+        if (h == 0 || tile + h * off < ntiles)
+          fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, (tile + h * off) * kTile, lane, lc);
     }
     return;
   } else {
@@ -627,14 +653,13 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
     uint32_t iter = 0;
     const uint32_t qs = (uint32_t)__cvta_generic_to_shared(q);
     for (uint64_t tile = first_tile; tile < ntiles; tile += step, ++iter) {
-      const uint64_t tile_b = tile + off;
-      uint32_t mask =
-          fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
-      if constexpr (PAIR) {
-        if (tile_b < ntiles)
-          mask |= fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile_b * kTile, lane, lc)
-                  << 16;
-      }
+      Mask mask = fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n, tile * kTile, lane, lc);
+#pragma unroll
+      for (int h = 1; h < NT; ++h)
+        if (tile + h * off < ntiles)
+          mask |= (Mask)fast_pass<DIST, COUNTED>(P, seed, ctr_base, sink, n,
+                                                 (tile + h * off) * kTile, lane, lc)
+                  << (16 * h);
       int total;
       bool multi;  // some lane holds two or more exceptions
       int slot = qn + warp_excl_mask(mask, lane, &total, &multi);
@@ -650,11 +675,11 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         // (practically never: ~100 exceptions in one tile, expected ~15) resolve
         // this tile's exceptions in place, each lane walking its own mask
         need_tables();
-        for (uint32_t m = mask; m; m &= m - 1) {
-          const int b = __ffs(m) - 1;
+        for (Mask m = mask; m; m &= m - 1) {
+          const int b = mask_top(m ^ (m & (m - 1)));  // lowest set bit
           resolve_one<DIST, COUNTED>(
               P, E, seed, ctr_base, sink,
-              ((b >> kPerLaneBits) ? tile_b : tile) * kTile +
+              (tile + (uint64_t)(b >> kPerLaneBits) * off) * kTile +
                   mask_bit_offset<Sink::V>(b & (kPerLane - 1), lane),
               lc);
         }
@@ -666,10 +691,11 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
         // every lane's highest entry with one predicated shared store (no
         // divergent block); the loop runs only when some lane holds two or
         // more (~40 % of tiles) and then only for the rest of the bits
-        const int hb = 31 - __clz(mask);
+        const int hb = mask_top(mask);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
                      "@p st.shared.u32 [%0], %1;\n\t}"
-                     ::"r"(qs + 4u * (uint32_t)slot), "r"(tag | (uint32_t)hb), "r"(mask)
+                     ::"r"(qs + 4u * (uint32_t)slot), "r"(tag | (uint32_t)hb),
+                     "r"((uint32_t)(mask != 0))
                      : "memory");
         if (multi) {
           if constexpr (DIST == ZF_EXP || (ZF_SECOND_STORE && PAIR)) {
@@ -678,26 +704,27 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
           // as well and the loop runs only for lanes with three or more.
           // (The unpaired normal kernel loses 6 % with it: +4 registers and
           // a worse layout.)
-          const uint32_t m2 = drop_top(mask);
-          const int hb2 = 31 - __clz(m2);
+          const Mask m2 = drop_top(mask);
+          const int hb2 = mask_top(m2);
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
                        "@p st.shared.u32 [%0], %1;\n\t}"
-                       ::"r"(qs + 4u * (uint32_t)(slot + 1)), "r"(tag | (uint32_t)hb2), "r"(m2)
+                       ::"r"(qs + 4u * (uint32_t)(slot + 1)), "r"(tag | (uint32_t)hb2),
+                       "r"((uint32_t)(m2 != 0))
                        : "memory");
           if (__ballot_sync(0xffffffffu, (m2 & (m2 - 1u)) != 0u)) {
             slot += 2;
-            for (uint32_t m = drop_top(m2); m;) {
-              const int b = 31 - __clz(m);
-              m ^= 1u << b;
+            for (Mask m = drop_top(m2); m;) {
+              const int b = mask_top(m);
+              m ^= (Mask)1 << b;
               ZF_CHECK(slot < kQueueCap);
             q[slot++] = tag | (uint32_t)b;
             }
           }
           } else {
           ++slot;
-          for (uint32_t m = drop_top(mask); m;) {
-            const int b = 31 - __clz(m);
-            m ^= 1u << b;
+          for (Mask m = drop_top(mask); m;) {
+            const int b = mask_top(m);
+            m ^= (Mask)1 << b;
             ZF_CHECK(slot < kQueueCap);
             q[slot++] = tag | (uint32_t)b;
           }
@@ -706,7 +733,7 @@ __device__ __forceinline__ void run_tiles(const DevPack& P, const DevPack& E, ui
       }
       qn += total;
 #if defined(ZF_CHECKS) && ZF_CHECKS
-      ZF_CHECK(qn <= kQueueCap && first_slot + __popc(mask) <= qn);
+      ZF_CHECK(qn <= kQueueCap && first_slot + mask_popc(mask) <= qn);
 #endif
       __syncwarp();
 #if defined(ZF_DEBUG_Q) && ZF_DEBUG_Q == 2  // cost isolation: scan + enqueue, no rounds
