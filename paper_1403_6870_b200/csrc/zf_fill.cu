@@ -211,6 +211,11 @@ static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* g
                         1, (ntiles + resident_warps * kTilesPerWarp / 2) /
                                (resident_warps * kTilesPerWarp));
   *grid = (int)std::min<uint64_t>(want, (uint64_t)per_sm * sm_count * waves);
+  // a queue entry holds a warp's loop iteration in 22 bits: never give a warp
+  // 2^21 or more tiles (only an enormous fill with ZF_GRID_WAVES set low could)
+  const uint64_t min_grid = (ntiles + (uint64_t)(threads / 32) * (1ull << 21) - 1) /
+                            ((uint64_t)(threads / 32) * (1ull << 21));
+  if ((uint64_t)*grid < min_grid) *grid = (int)std::min<uint64_t>(min_grid, want);
   if (*grid < 1) *grid = 1;
   return ZF_OK;
 }
