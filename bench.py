@@ -487,7 +487,19 @@ def main():
         for _ in range(p_steps):
             e2e_s.fill(arr)
         dtp = time.perf_counter() - t
-        dt, dtp = max_over_ranks([dt, dtp])
+        # the host link's own D2H rate (a plain pinned copy of the same bytes
+        # from HBM), so the e2e number can be read against its bound
+        dev_buf = out[:m]
+        for _ in range(2):
+            host.copy_(dev_buf, non_blocking=True)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(3):
+            host.copy_(dev_buf, non_blocking=True)
+        torch.cuda.synchronize()
+        dtl = (time.perf_counter() - t) / 3
+        dt, dtp, dtl = max_over_ranks([dt, dtp, dtl])
+        link_gbs = 8 * m / dtl / 1e9
         e2e = {"value": m * world * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": 8 * m, "steps": args.steps, "n_per_step": m,
                "note": "NormalSampler.fill(pinned host tensor), every step: device generation + "
@@ -497,7 +509,12 @@ def main():
                             "note": "NormalSampler.fill(np.empty(2^28)) repeatedly into the same "
                                     "array, the reference's own usage (exponential.py:45-50): "
                                     "the array is page-locked in place by the first (untimed) "
-                                    "call and DMA'd into directly"}}
+                                    "call and DMA'd into directly"},
+               "link_d2h_gbs_per_gpu": link_gbs,
+               "frac_of_link": (m * args.steps / dt) * 8 / 1e9 / link_gbs,
+               "link_note": "a pinned cudaMemcpy D2H of the same 8*n bytes on this box: the "
+                            "PCIe bound of any host-destination fill (fp64 samples/s <= "
+                            "link GB/s / 8 per GPU)"}
         del host
 
     if rank == 0:
