@@ -315,6 +315,61 @@ __global__ void rp_mark(const uint32_t* __restrict__ E, const uint32_t* __restri
   }
 }
 
+// Stages C and D in one CTA for short exceptional lists (m <= kSmallResolve,
+// e.g. config 1's ~17 k): the reach prefix-max, heads, cluster walks and
+// interior counts without four launches and two scans.  Also zeroes the
+// per-block counts it accumulates into.
+constexpr uint32_t kSmallResolve = 1u << 17;
+__global__ void __launch_bounds__(1024)
+    rp_resolve_small(const uint32_t* __restrict__ E, const uint32_t* __restrict__ len,
+                     const uint32_t* __restrict__ pm, uint64_t L, uint8_t* __restrict__ real,
+                     uint32_t* __restrict__ block_int, uint32_t* __restrict__ spill, uint32_t nb) {
+  __shared__ uint64_t wb[32];
+  __shared__ uint32_t headbits[kSmallResolve / 32];
+  const uint32_t m = min(*pm, kSmallResolve);
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    block_int[b] = 0;
+    spill[b] = 0;
+  }
+  for (uint32_t w = threadIdx.x; w < (m + 31) / 32; w += blockDim.x) headbits[w] = 0;
+  const uint32_t per = (m + blockDim.x - 1) / blockDim.x;
+  const uint32_t beg = min(m, threadIdx.x * per), end = min(m, beg + per);
+  uint64_t mx = 0;
+  for (uint32_t i = beg; i < end; ++i) mx = max(mx, reach_of(E, len, i));
+  // (block_exclusive synchronises, so the zeroing above is complete after it)
+  uint64_t run = block_exclusive<uint64_t>(mx, 0ull, Max(), wb, nullptr);
+  for (uint32_t i = beg; i < end; ++i) {  // heads: not covered by an earlier candidate
+    if (run <= E[i]) atomicOr(&headbits[i >> 5], 1u << (i & 31));
+    run = max(run, reach_of(E, len, i));
+  }
+  __syncthreads();
+  auto head = [&](uint32_t i) { return (headbits[i >> 5] >> (i & 31)) & 1u; };
+  // walks: a thread walks every cluster whose head lies in its range, into the
+  // next thread's range if the cluster runs on
+  {
+    uint32_t i = beg;
+    while (i < end && !head(i)) ++i;
+    uint64_t cursor = 0;
+    for (; i < m && (i < end || !head(i)); ++i) {
+      const uint8_t r = E[i] >= cursor;
+      real[i] = r;
+      if (r) cursor = reach_of(E, len, i);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = beg; i < end; ++i) {  // interior counts per emit block (rp_mark)
+    if (!real[i]) continue;
+    const uint64_t p = E[i];
+    const uint64_t stop = len[i] == kIncomplete ? L : std::min<uint64_t>(p + len[i], L);
+    for (uint64_t q = p + 1; q < stop;) {
+      const uint64_t b = q / kRB, e = std::min<uint64_t>(stop, (b + 1) * kRB);
+      atomicAdd(block_int + b, (uint32_t)(e - q));
+      if (q == b * kRB) spill[b] = (uint32_t)(e - q);
+      q = e;
+    }
+  }
+}
+
 // start positions per emit block = block length - interior words
 __global__ void rp_block_starts(const uint32_t* __restrict__ block_int, uint32_t nb, uint64_t L,
                                 uint32_t* __restrict__ starts) {
@@ -958,6 +1013,7 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
     rp_compact_exc<DIST><<<nb, kRT, 0, s>>>(win, dP, boff, E, cap);
   }
   dbg("compact", s);
+  const bool small_resolve = cap <= kSmallResolve;
   if (cap) {
     constexpr int kPacks = kPacksOf<DIST>;
     const size_t smem = kPacks * sizeof(DevPack);
@@ -965,6 +1021,11 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
                                 (int)smem));
     rp_draw_exc<DIST><<<(cap + kRT - 1) / kRT, kRT, smem, s>>>(t->dev, win, E, dm, eo);
     dbg("rp_draw_exc<DIST>", s);
+  }
+  if (small_resolve) {
+    rp_resolve_small<<<1, 1024, 0, s>>>(E, eo.len, dm, L, real, bcnt, spill, nb);
+    dbg("rp_resolve_small", s);
+  } else {
     rp_reach_max<<<nbE, kRT, 0, s>>>(E, eo.len, dm, bmax);
     dbg("rp_reach_max", s);
     ZF_TRY_STATUS(scan_n<uint64_t>(ws, bmax, bpre, nbE, Max(), 0ull, nullptr, s));
@@ -974,11 +1035,11 @@ int replay_window(const zf_tables* t, const Window& win, void* out, uint64_t n, 
     const uint64_t walkers = (cap + kWalkChunk - 1) / kWalkChunk;
     rp_walk<<<(uint32_t)((walkers + kRT - 1) / kRT), kRT, 0, s>>>(E, eo.len, head, dm, real);
     dbg("rp_walk", s);
+    ZF_TRY(cudaMemsetAsync(bcnt, 0, nb * sizeof(uint32_t), s));  // reused: interior per block
+    ZF_TRY(cudaMemsetAsync(spill, 0, nb * sizeof(uint32_t), s));
+    rp_mark<<<(cap + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, dm, L, bcnt, spill);
+    dbg("rp_mark", s);
   }
-  ZF_TRY(cudaMemsetAsync(bcnt, 0, nb * sizeof(uint32_t), s));  // reused: interior per block
-  ZF_TRY(cudaMemsetAsync(spill, 0, nb * sizeof(uint32_t), s));
-  if (cap) rp_mark<<<(cap + kRT - 1) / kRT, kRT, 0, s>>>(E, eo.len, real, dm, L, bcnt, spill);
-  dbg("rp_mark", s);
   ZF_TRY_STATUS((scan_n<uint32_t, Add, true>(ws, bcnt, boff2, nb, Add(), 0u, nullptr, s, 0,
                                              nullptr, L, bcnt2)));
   dbg("block starts", s);
