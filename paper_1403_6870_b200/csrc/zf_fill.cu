@@ -18,7 +18,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <new>
 #include <type_traits>
 #include <vector>
@@ -177,13 +179,30 @@ template <typename K>
 static int grid_for(K kernel, size_t smem, int sm_count, uint64_t ntiles, int* grid,
                     int fixed_waves = 0, int threads = kThreads, bool paired = false) {
   static_assert(sizeof(K) > 0, "");
+  // the shared-memory attribute and the occupancy query once per (device,
+  // kernel, shared memory): ~5 us of driver calls a small fill would pay on
+  // every launch
+  int dev = 0;
+  ZF_TRY(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), smem, threads);
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t, int>, int> cache;
   int per_sm = 0;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-  if (e != cudaSuccess) return (int)e;
-  per_sm = std::max(per_sm, 1);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) per_sm = it->second;
+  }
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (e != cudaSuccess) return (int)e;
+    per_sm = std::max(per_sm, 1);
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = per_sm;
+  }
   const uint64_t want = (ntiles + threads / 32 - 1) / (threads / 32);
   // ZF_GRID_WAVES=w overrides the number of resident waves per launch.  By
   // default every warp gets ~kTilesPerWarp tiles: a warp that walks hundreds
