@@ -72,6 +72,19 @@ def test_xoshiro_jump_matches_stepping(built_lib, orc):
         assert np.array_equal(st, ref), (seed, k)
 
 
+def test_xoshiro_jump_composes_for_large_distances(built_lib, orc):
+    """Jumps by distances far beyond stepping reach (the high bits of k go
+    through the precomputed x^(2^i) powers): jump(a) then jump(b) == jump(a + b)."""
+    from paper_1403_6870_b200 import _lib
+    for a, b in ((2**40 + 3, 2**33 + 7), (2**63 - 1, 2**62 + 12345), (999_983, 2**50)):
+        s1 = orc.xoshiro_state(9)
+        _lib.check(built_lib.zf_xoshiro_jump(_lib.u64p(s1), a))
+        _lib.check(built_lib.zf_xoshiro_jump(_lib.u64p(s1), b))
+        s2 = orc.xoshiro_state(9)
+        _lib.check(built_lib.zf_xoshiro_jump(_lib.u64p(s2), a + b))
+        assert np.array_equal(s1, s2), (a, b)
+
+
 def test_published_jump_polynomial(built_lib):
     """x^(2^128) mod P is xoshiro256's published jump() constant: the
     characteristic polynomial recovered by Berlekamp-Massey is right."""
