@@ -13,6 +13,9 @@
 //   pass 2 (rare):  the flagged samples are queued per warp across tiles and
 //                   resolved 32 at a time (one per lane) on their secondary
 //                   counter streams; results patch lines still held in L2.
+// The modified fp64 fills (and the fp32 exponential) run pass 1 on two
+// adjacent tiles before one round of queue bookkeeping; the grid gives every
+// warp ~32 tiles (round-2 log).
 #include <cuda_runtime.h>
 
 #include <algorithm>

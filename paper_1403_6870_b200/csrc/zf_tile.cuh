@@ -8,7 +8,9 @@
 //           set a bit in the lane's mask.
 //   pass 2  the warp compacts the masked samples into a per-warp smem queue
 //           that persists across tiles and resolves them in full rounds of 32
-//           (one sample per lane) once 32 are queued.
+//           (one sample per lane) once 32 are queued.  Callers may run pass 1
+//           on 2 (or 4) tiles before one round of this bookkeeping
+//           (run_tiles<..., NT>: the lane masks side by side in one mask).
 // A "sink" decides what happens to each value: StoreSink writes it to HBM
 // (128-bit vector stores in pass 1, 8-byte patches in pass 2 to lines that are
 // still L2-resident), StatsSink folds it into moment sums / histogram /
