@@ -401,7 +401,7 @@ struct EmitArgs {
 };
 
 #ifndef ZF_EMIT_MINB
-#define ZF_EMIT_MINB 6  // 40 registers: occupancy hides the load latency
+#define ZF_EMIT_MINB 8  // 32 registers (a few bytes of stack): occupancy hides the load latency
 #endif
 // FULL = false: plain fills (no path records, no counters) -- the default
 // oracle-mode call; its per-position code keeps no counter or record state.
