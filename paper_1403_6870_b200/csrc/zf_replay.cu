@@ -455,22 +455,33 @@ __global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
     }
   }
   __syncthreads();
-  uint8_t inter[kRI];
-#pragma unroll
-  for (int j = 0; j < kRI; ++j) {
-    const uint32_t p = p0 + 32u * j;
-    const uint32_t r = p - b0;
-    inter[j] = p < L32 ? (uint8_t)((imap[r >> 5] >> (r & 31)) & 1u) : 1;
-  }
-  uint32_t be[kRI], bs[kRI];
+  // item j of this warp is the 32 positions of bitmap word wid * kRI + j (lane
+  // = bit), so the warp's start ballot is that word complemented: one
+  // broadcast LDS per item, no per-lane bit extraction
+  const uint32_t wid = threadIdx.x >> 5;
+  const uint32_t pw0 = b0 + wid * (uint32_t)kWarpSpan;
+  // (the start ballot is re-read in the emit loop rather than kept: the plain
+  // kernel runs at 32 registers)
+  auto start_bits = [&](int j) -> uint32_t {
+    const uint32_t pw = pw0 + 32u * j;  // first position of the item's 32
+    // in-window lanes: the low min(L - pw, 32) bits, branch-free
+    const uint32_t dd = pw >= L32 ? 0u : min(L32 - pw, 32u);
+    return ~imap[wid * kRI + j] & __funnelshift_lc(0xFFFFFFFFu, 0u, dd);
+  };
+  uint32_t be[kRI];
   uint32_t ce = 0, cs = 0;
+  [[maybe_unused]] const uint32_t lmx = (uint32_t)P->lmax;
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const bool in = p0 + 32u * j < L32;
-    be[j] = __ballot_sync(0xffffffffu, in && exc_word<DIST>(*P, wds[j]));
-    bs[j] = __ballot_sync(0xffffffffu, inter[j] == 0);
+    const bool in = pw0 + 32u * j + lane < L32;
+    bool exc;
+    if constexpr (kTrad<DIST>)
+      exc = exc_word<DIST>(*P, wds[j]);
+    else
+      exc = ((uint32_t)wds[j] & 0xFFu) >= lmx;
+    be[j] = __ballot_sync(0xffffffffu, in && exc);
     ce += __popc(be[j]);
-    cs += __popc(bs[j]);
+    cs += __popc(start_bits(j));
   }
   uint32_t eidx, rank;
   warp_base2(ce, cs, wb, &eidx, &rank);
@@ -480,8 +491,9 @@ __global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < kRI; ++j) {
-    const bool is_ex = (be[j] >> lane) & 1, is_st = (bs[j] >> lane) & 1;
-    const uint32_t e_i = eidx + __popc(be[j] & lt), r_i = rank + __popc(bs[j] & lt);
+    const uint32_t bs = start_bits(j);
+    const bool is_ex = (be[j] >> lane) & 1, is_st = (bs >> lane) & 1;
+    const uint32_t e_i = eidx + __popc(be[j] & lt), r_i = rank + __popc(bs & lt);
     if (is_st && r_i < n32 && !(is_ex && e_i >= m)) {
       const uint32_t p = p0 + 32u * j;
       double v;
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(kRT, FULL ? 4 : ZF_EMIT_MINB)
       }
     }
     eidx += __popc(be[j]);
-    rank += __popc(bs[j]);
+    rank += __popc(bs);
   }
   if (FULL && a.counters) {  // counted fills only: 6 atomics per warp on 6 addresses
     for (int q = 0; q < 6; ++q) {
