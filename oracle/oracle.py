@@ -67,6 +67,9 @@ def lib():
         L.orc_fill_sharded_chunked.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
                                                C.c_uint64, C.c_int, C.c_uint64,
                                                C.POINTER(C.c_double)]
+        L.orc_check_ctr.restype = C.c_int64
+        L.orc_check_ctr.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                    C.c_void_p, C.c_int, C.c_uint64, C.c_int, u64p]
         L.orc_fill_sharded.restype = C.c_int
         L.orc_fill_sharded.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                        C.c_uint64, C.c_int]
@@ -246,6 +249,24 @@ def fill_ctr(dist, n: int, seed: int, ctr_base: int = 0, records=False):
     lib().orc_fill_ctr(_dist(dist), C.byref(h.c), C.byref(e.c), seed & (2**64 - 1), ctr_base,
                        _ptr(out), n, _ptr(cnt), _ptr(recs) if recs is not None else None)
     return out, cnt, recs
+
+
+def check_ctr(dist, got: np.ndarray, seed: int, ctr_base: int = 0,
+              threads: int | None = None) -> tuple[int, int]:
+    """Compare EVERY sample of a production fill (float64 or float32, C-contiguous)
+    with the oracle, in place and on `threads` host threads (default: all of
+    them).  Returns (number of mismatching samples, lowest mismatching index or
+    len(got))."""
+    if got.dtype not in (np.float64, np.float32) or not got.flags.c_contiguous:
+        raise ValueError("check_ctr needs a contiguous float64/float32 array")
+    h, e = packs(dist)
+    threads = threads or len(os.sched_getaffinity(0))
+    first = C.c_uint64()
+    bad = lib().orc_check_ctr(_dist(dist), C.byref(h.c), C.byref(e.c), seed & (2**64 - 1),
+                              ctr_base, _ptr(got), int(got.dtype == np.float32), got.size,
+                              threads, C.byref(first))
+    assert bad >= 0
+    return int(bad), int(first.value)
 
 
 def ctr_words(seed: int, K: int, m: int) -> np.ndarray:

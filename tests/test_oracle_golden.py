@@ -90,6 +90,31 @@ def test_config1_values_and_paths(orc, golden, dist):
 
 
 @pytest.mark.parametrize("dist", ["exp", "normal"])
+def test_whole_output_checker_is_the_production_oracle(orc, golden, dist):
+    """`check_ctr` (the multi-threaded in-place comparison the full-size GPU
+    parity test uses) accepts the reference-evaluated production goldens and
+    `fill_ctr`'s output in fp64 and fp32, and reports injected bit flips with
+    the lowest index, whatever the thread split."""
+    for key, want in golden[f"ctr_{dist}"].items():
+        seed, base = (int(x) for x in key.split(":"))
+        vals = hex_to_bits(want).view(np.float64)
+        assert orc.check_ctr(dist, vals, seed, base) == (0, len(want)), key
+    n = 300_007
+    base = (1 << 40) + 11
+    want, _, _ = orc.fill_ctr(dist, n, seed=7, ctr_base=base)
+    for threads in (1, 3, 16):
+        assert orc.check_ctr(dist, want, 7, base, threads=threads) == (0, n)
+        assert orc.check_ctr(dist, want.astype(np.float32), 7, base, threads=threads) == (0, n)
+    assert orc.check_ctr(dist, want, 8, base)[0] > n // 2  # another seed: nothing matches
+    exc = np.flatnonzero(np.isin(np.arange(n), [5, 77_777, n - 1]))
+    flipped = want.copy()
+    flipped.view(np.uint64)[exc] ^= np.uint64(1)
+    for threads in (1, 5):
+        assert orc.check_ctr(dist, flipped, 7, base, threads=threads) == (3, 5)
+    assert orc.check_ctr(dist, want[:0], 7, base) == (0, 0)
+
+
+@pytest.mark.parametrize("dist", ["exp", "normal"])
 def test_production_stream_matches_reference_replay(orc, golden, dist):
     """The counter ("ctr") stream restated in C equals the reference run over
     each sample's word sequence."""
