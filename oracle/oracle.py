@@ -70,6 +70,10 @@ def lib():
         L.orc_check_ctr.restype = C.c_int64
         L.orc_check_ctr.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                     C.c_void_p, C.c_int, C.c_uint64, C.c_int, u64p]
+        L.orc_count_ctr.restype = C.c_int
+        L.orc_count_ctr.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                    C.c_uint64, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int,
+                                    u64p]
         L.orc_fill_sharded.restype = C.c_int
         L.orc_fill_sharded.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                        C.c_uint64, C.c_int]
@@ -267,6 +271,21 @@ def check_ctr(dist, got: np.ndarray, seed: int, ctr_base: int = 0,
                               threads, C.byref(first))
     assert bad >= 0
     return int(bad), int(first.value)
+
+
+def count_ctr(dist, n: int, seed: int, ctr_base: int = 0, thresholds=(), abs_thresh=False,
+              threads: int | None = None) -> list[int]:
+    """Counts of x > t (|x| > t) over `n` production draws, nothing stored
+    (config 5's generate-and-count), on `threads` host threads."""
+    h, e = packs(dist)
+    threads = threads or len(os.sched_getaffinity(0))
+    t = np.asarray(thresholds, dtype=np.float64)
+    counts = np.zeros(max(len(t), 1), dtype=np.uint64)
+    rc = lib().orc_count_ctr(_dist(dist), C.byref(h.c), C.byref(e.c), seed & (2**64 - 1),
+                             ctr_base, n, t.ctypes.data_as(C.POINTER(C.c_double)), len(t),
+                             int(abs_thresh), threads, _u64p(counts))
+    assert rc == 0
+    return [int(c) for c in counts[:len(t)]]
 
 
 def ctr_words(seed: int, K: int, m: int) -> np.ndarray:

@@ -98,3 +98,20 @@ def test_the_check_sees_single_bit_flips(zf, orc, cuda, dtype):
     n = (1 << 29) + 5
     flips = (CHUNK - 1, 3 * CHUNK, n - 1)
     assert _check_whole(zf, orc, cuda, "normal", dtype, n, 99, 0, corrupt=flips) == (3, CHUNK - 1)
+
+
+def test_config5_share_counts_equal_the_oracle(zf, orc, cuda):
+    """BASELINE config 5, one GPU's share at 8 GPUs (2^33 N(0,1) + 2^33 Exp(1)
+    draws, seed 99, rank 3's counter range): the in-kernel tail counts
+    (|x| > 5, 6, 7; x > X[1]) equal the CPU oracle's over the same draws."""
+    from paper_1403_6870_b200 import scale, shard
+    from paper_1403_6870_b200.tables import default_tables
+    m = _full_n() * 2
+    base = shard.counter_base(3)
+    x1 = float(default_tables("exponential").x[1])
+    got_n = scale.device_counts("normal", scale.C5_SEED, base, m, scale.C5_THRESH, True,
+                                device=cuda)
+    got_e = scale.device_counts("exp", scale.C5_SEED, base, m, (x1,), False, device=cuda)
+    assert [int(c) for c in got_n] == orc.count_ctr("normal", m, scale.C5_SEED, base,
+                                                   scale.C5_THRESH, True)
+    assert [int(c) for c in got_e] == orc.count_ctr("exp", m, scale.C5_SEED, base, (x1,), False)

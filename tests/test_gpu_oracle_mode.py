@@ -151,6 +151,22 @@ def test_long_stream_many_windows(zf, orc, cuda, dist):
     assert np.array_equal(bits(got), bits(want))
 
 
+@pytest.mark.parametrize("dist", DISTS)
+def test_config2_sized_stream_every_sample(zf, orc, cuda, dist):
+    """The reference's own xoshiro256++ stream at BASELINE config 2's size
+    (n = 2^28, 2 GiB): every sample of one `fill` against the sequential CPU
+    oracle, then the stream continues where the reference's would."""
+    n = 1 << 28
+    seed = orc.derive_seed(1234, 0)  # what fill_sharded's only thread seeds with
+    s = cls_of(zf, dist)(source=zf.UniformSource(seed), device=cuda)
+    got = s.fill(n).cpu().numpy()
+    tail = s.fill(1000).cpu().numpy()
+    want = orc.fill_sharded(dist, n + 1000, 1234, threads=1)
+    diff = np.flatnonzero(bits(got) != bits(want[:n]))
+    assert diff.size == 0, f"{diff.size} mismatches, first at {int(diff[0])}"
+    assert np.array_equal(bits(tail), bits(want[n:]))
+
+
 def test_adversarial_replay_all_exceptional(zf, orc, cuda):
     """Every word exceptional (byte 255): long overlapping draw chains."""
     rng = np.random.default_rng(0)

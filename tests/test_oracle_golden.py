@@ -114,6 +114,21 @@ def test_whole_output_checker_is_the_production_oracle(orc, golden, dist):
     assert orc.check_ctr(dist, want[:0], 7, base) == (0, 0)
 
 
+@pytest.mark.parametrize("dist,thr,use_abs", [("normal", (0.0, 1.0, 3.0, 3.7, 5.0), True),
+                                              ("normal", (-1.0, 0.0, 2.5), False),
+                                              ("exp", (0.5, 7.569274694148063, 9.0), False)])
+def test_generate_and_count_is_the_production_oracle(orc, dist, thr, use_abs):
+    """`count_ctr` (config 5's generate-and-count on the CPU, nothing stored)
+    counts exactly what numpy counts on `fill_ctr`'s values, for any thread split."""
+    n, base = 1_000_003, (5 << 40) + 9
+    vals, _, _ = orc.fill_ctr(dist, n, seed=99, ctr_base=base)
+    a = np.abs(vals) if use_abs else vals
+    want = [int((a > t).sum()) for t in thr]
+    for threads in (1, 7):
+        assert orc.count_ctr(dist, n, 99, base, thr, use_abs, threads=threads) == want
+    assert orc.count_ctr(dist, 0, 99, base, thr, use_abs) == [0] * len(thr)
+
+
 @pytest.mark.parametrize("dist", ["exp", "normal"])
 def test_production_stream_matches_reference_replay(orc, golden, dist):
     """The counter ("ctr") stream restated in C equals the reference run over
