@@ -206,7 +206,9 @@ int zf_fill_replay(const zf_tables* t, int dist, int dtype, const uint64_t* word
  * with host `state` updated in place exactly as `fill_exp(state, gid, ...)`
  * would (gid 0: xoshiro256++ state[4]; gid 1: splitmix64 state[1];
  * gid 2: state[0] = cursor, replay words in replay_words_dev/nwords;
- * gid 3: {seed, counter}).  Synchronises `stream` for gid 0..2. */
+ * gid 3: {seed, counter}).  Synchronises `stream` for gid 0..2.  Any n:
+ * fills above 2^28 samples are resolved window by window inside the call
+ * (with recs_dev, n must stay below 2^31: ZF_ERANGE otherwise). */
 int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* state,
                 const uint64_t* replay_words_dev, uint64_t nwords, void* out_dev, uint64_t n,
                 zf_path_rec* recs_dev, int64_t* counters_dev, void* stream);

@@ -281,6 +281,23 @@ int zf_fill_gid(const zf_tables* t, int dist, int dtype, int gid, uint64_t* stat
     return ZF_OK;
   }
   if (n == 0) return ZF_OK;
+  // One window resolves fewer than 2^31 samples (32-bit positions): a larger
+  // fill goes chunk by chunk, each continuing the stream where the previous
+  // one stopped, exactly like consecutive fills.  (Per-sample records count
+  // their start words from the call's first word, so a recorded fill stays
+  // one window.)
+  constexpr uint64_t kGidChunk = 1ull << 28;
+  if (n > kGidChunk && !recs_dev) {
+    if (!out_dev) return ZF_EINVAL;
+    const size_t esz = dtype == ZF_F32 ? 4 : 8;
+    for (uint64_t off = 0; off < n; off += kGidChunk) {
+      const uint64_t m = n - off < kGidChunk ? n - off : kGidChunk;
+      ZF_TRY_STATUS(zf_fill_gid(t, dist, dtype, gid, state, replay_words_dev, nwords,
+                                static_cast<unsigned char*>(out_dev) + off * esz, m, nullptr,
+                                counters_dev, stream));
+    }
+    return ZF_OK;
+  }
   uint64_t consumed = 0;
   if (gid == ZF_GEN_REPLAY) {
     ZF_TRY_STATUS(run_replay(t, dist, dtype, replay_words_dev, nwords, state[0], 1, out_dev, n,

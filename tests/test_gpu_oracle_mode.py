@@ -167,6 +167,44 @@ def test_config2_sized_stream_every_sample(zf, orc, cuda, dist):
     assert np.array_equal(bits(tail), bits(want[n:]))
 
 
+def test_fill_above_one_window_continues_the_stream(zf, orc, cuda):
+    """A single oracle-mode fill larger than the C-ABI's 2^28-sample window
+    chunk (the reference has no size limit): the chunks continue one stream --
+    checked on the chunk boundary, the end, the continuation and the counters
+    of a counted fill against the sequential oracle."""
+    n = (1 << 28) + 1_000_003
+    seed = orc.derive_seed(5, 0)
+    s = zf.ExpSampler(source=zf.UniformSource(seed), device=cuda)
+    got = s.fill_counted(n)
+    tail = s.fill(512).cpu().numpy()
+    want = orc.fill_sharded("exp", n + 512, 5, threads=1)
+    for lo, hi in ((0, 4096), ((1 << 28) - 4096, (1 << 28) + 4096), (n - 4096, n)):
+        assert np.array_equal(bits(got[lo:hi].cpu().numpy()), bits(want[lo:hi])), lo
+    assert np.array_equal(bits(tail), bits(want[n:]))
+    _, cnt, _, _ = orc.fill_stream("exp", n, seed=seed)
+    assert s.path_counts.as_tuple() == tuple(int(v) for v in cnt)
+
+
+def test_fill_of_more_than_2p31_samples(zf, orc, cuda):
+    """n above the 32-bit window positions (the old ZF_ERANGE): the last sample
+    of a 2^31 + 5 sample N(0,1) fill equals the sequential oracle's (which
+    keeps only a small buffer), so all eight chunks consumed the right words."""
+    import torch
+    n = (1 << 31) + 5
+    free, _ = torch.cuda.mem_get_info(cuda)
+    if free < 8 * n + (8 << 30):
+        pytest.skip("not enough device memory")
+    seed = orc.derive_seed(11, 0)
+    out = zf.NormalSampler(source=zf.UniformSource(seed), device=cuda).fill(n)
+    last = out[-1].item()
+    first = out[:1000].cpu().numpy()
+    del out
+    torch.cuda.empty_cache()
+    assert bits(np.array([last]))[0] == bits(np.array([orc.fill_sharded_chunked(
+        "normal", n, 11, threads=1)]))[0]
+    assert np.array_equal(bits(first), bits(orc.fill_sharded("normal", 1000, 11, threads=1)))
+
+
 def test_adversarial_replay_all_exceptional(zf, orc, cuda):
     """Every word exceptional (byte 255): long overlapping draw chains."""
     rng = np.random.default_rng(0)
