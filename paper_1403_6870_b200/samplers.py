@@ -256,7 +256,14 @@ class _SamplerBase:
         if isinstance(out, torch.Tensor) and out.is_cuda:
             if out.device != self.device:
                 raise ValueError(f"output on {out.device}, sampler on {self.device}")
-            self._launch(out.view(-1) if out.is_contiguous() else out, counted)
+            if out.is_contiguous():
+                self._launch(out.view(-1), counted)
+            else:
+                # a strided view (the reference's kernels index out[k] through any
+                # strides): draw into a dense buffer, scatter in element order
+                tmp = torch.empty(out.shape, dtype=out.dtype, device=self.device)
+                self._launch(tmp.view(-1), counted)
+                out.copy_(tmp)
             return out
         # host destination: numpy array or CPU tensor -> through the device in chunks
         if isinstance(out, np.ndarray) and out.flags.c_contiguous:
@@ -265,7 +272,12 @@ class _SamplerBase:
         if not isinstance(host, torch.Tensor) or host.is_cuda:
             raise TypeError("out must be an int, a CUDA tensor, a numpy array or a CPU tensor")
         if not host.is_contiguous():
-            raise ValueError("host output must be contiguous")
+            # strided host views work in the reference (numba indexes out[k]):
+            # fill a dense array, then assign in element order
+            dense = torch.empty(host.shape, dtype=host.dtype)
+            self._fill_host(dense.view(-1), counted)
+            host.copy_(dense)
+            return out
         self._fill_host(host.view(-1), counted)
         return out
 

@@ -83,8 +83,19 @@ def test_misaligned_and_strided_views(zf, orc, cuda, dist):
     want, _, _ = orc.fill_ctr(dist, 10_000, seed=3)
     assert_bits_equal(view.cpu().numpy(), bits(want))
     assert buf[0].item() == 0.0
-    with pytest.raises(ValueError):
-        sampler(zf, dist, 3, device=cuda).fill(buf[::2])
+    # strided views, device and host (the reference's kernels write out[k]
+    # through any strides): values land in element order, the gaps untouched
+    buf.zero_()
+    r = sampler(zf, dist, 3, device=cuda).fill(buf[::2])
+    assert r.data_ptr() == buf.data_ptr() and r.numel() == 5001
+    want5, _, _ = orc.fill_ctr(dist, 5001, seed=3)
+    assert_bits_equal(buf[::2].cpu().numpy(), bits(want5))
+    assert not buf[1::2].any().item()
+    host = np.zeros((300, 4))
+    col = host[:, 1]
+    assert sampler(zf, dist, 3, device=cuda).fill(col) is col
+    assert_bits_equal(host[:, 1], bits(want5[:300]))
+    assert not host[:, [0, 2, 3]].any()
 
 
 @pytest.mark.parametrize("dist", DISTS)
