@@ -174,7 +174,10 @@ int zf_tables_destroy(zf_tables* t);
  *   S(c) = fmix64(seed + (c+1)*0x9E3779B97F4A7C15)   (MurmurHash3's 64-bit
  *          finalizer on splitmix64's Weyl sequence; the draw body is the
  *          reference's, so any sample can be replayed through it).
- * ctr_base + n must not exceed 2^44.  Asynchronous on `stream`.
+ * ctr_base + n must not exceed 2^44.  Asynchronous on `stream`: one kernel
+ * launch, no allocation, synchronisation or host round trip, so the call
+ * (like zf_batch_fill) may be captured into a CUDA graph; a replay redoes the
+ * captured (seed, ctr_base) range.
  * counters_dev (nullable): int64[6] accumulated with the reference's slots. */
 int zf_fill(const zf_tables* t, int dist, int dtype, uint64_t seed, uint64_t ctr_base,
             void* out_dev, uint64_t n, int64_t* counters_dev, void* stream);

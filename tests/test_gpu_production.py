@@ -228,6 +228,47 @@ def test_batch_plan_resident_refills(zf, orc, cuda):
         assert np.array_equal(bits(host[off:off + n]), bits(want)), (dist, n, seed)
 
 
+def test_production_launches_capture_into_cuda_graphs(zf, orc, cuda):
+    """`zf_fill` (fp64, fp32) and `zf_batch_fill` are plain launches on the caller's
+    stream -- no allocation, synchronisation or host round trip -- so a
+    launch-bound inner loop can live in a CUDA graph ("batch
+    into one launch/graph").  A replay redoes the captured (seed, counter)
+    ranges: the graph's outputs equal the oracle after every replay."""
+    import torch
+    n = 200_003
+    outs = {d: torch.empty(n, dtype=torch.float64, device=cuda) for d in DISTS}
+    f32 = torch.empty(n, dtype=torch.float32, device=cuda)
+    reqs = [("exp" if i % 2 else "normal", 8192, 900 + i) for i in range(64)]
+    plan = zf.BatchPlan([r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs])
+    bout = torch.empty(plan.total, dtype=torch.float64, device=cuda)
+    plan.fill(out=bout, device=cuda)  # the plan's device image exists before the capture
+    samplers = {d: sampler(zf, d, 77, 1 << 40, device=cuda) for d in DISTS}
+    s32 = sampler(zf, "normal", 78, device=cuda)
+    torch.cuda.synchronize(cuda)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for d in DISTS:
+            samplers[d].fill(outs[d])
+        s32.fill(f32)
+        plan.fill(out=bout, device=cuda)
+    for rep in range(3):
+        for t in (*outs.values(), f32, bout):
+            t.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize(cuda)
+        for d in DISTS:
+            want, _, _ = orc.fill_ctr(d, n, seed=77, ctr_base=1 << 40)
+            assert_bits_equal(outs[d].cpu().numpy(), bits(want), f"graph {d} replay {rep}")
+        want, _, _ = orc.fill_ctr("normal", n, seed=78)
+        assert np.array_equal(f32.cpu().numpy(), want.astype(np.float32))
+        host = bout.cpu().numpy()
+        for (dist, m, seed), off in zip(reqs, plan.offsets):
+            want, _, _ = orc.fill_ctr(dist, m, seed=seed)
+            assert np.array_equal(bits(host[off:off + m]), bits(want)), (dist, seed, rep)
+    # the samplers' host-side counters advanced once, at capture time
+    assert int(samplers["exp"].source.state[1]) == (1 << 40) + n
+
+
 def test_convenience_api(zf, cuda):
     zf.seed(2024)
     a = zf.normal(1000, device=cuda)
