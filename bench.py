@@ -473,9 +473,12 @@ def main():
         torch.cuda.synchronize()
         if barrier:
             barrier()
+        step_s = []
         t = time.perf_counter()
         for _ in range(args.steps):
-            e2e_s.fill(host)
+            t1 = time.perf_counter()
+            e2e_s.fill(host)  # returns when the last chunk's copy has landed
+            step_s.append(time.perf_counter() - t1)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         arr = np.empty(m)
@@ -502,6 +505,8 @@ def main():
         link_gbs = 8 * m / dtl / 1e9
         e2e = {"value": m * world * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": 8 * m, "steps": args.steps, "n_per_step": m,
+               "step_ms": {"min": 1e3 * min(step_s), "median": 1e3 * float(np.median(step_s)),
+                           "max": 1e3 * max(step_s)},
                "note": "NormalSampler.fill(pinned host tensor), every step: device generation + "
                        "D2H copy of the step's 2^28 samples (double-buffered chunks); the input "
                        "is a seed passed by value (no H2D bytes)",
