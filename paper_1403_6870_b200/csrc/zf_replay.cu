@@ -348,9 +348,12 @@ __global__ void __launch_bounds__(1024)
   // next thread's range if the cluster runs on
   {
     uint32_t i = beg;
-    while (i < end && !head(i)) ++i;
+    while (i < end && !head(i)) ++i;  // leading non-heads belong to an earlier walker
+    // (a range without a head starts no walk: stepping on from `end` with an
+    // empty cursor would race the earlier walker's flags with wrong ones)
+    const bool walks = i < end;
     uint64_t cursor = 0;
-    for (; i < m && (i < end || !head(i)); ++i) {
+    for (; walks && i < m && (i < end || !head(i)); ++i) {
       const uint8_t r = E[i] >= cursor;
       real[i] = r;
       if (r) cursor = reach_of(E, len, i);
