@@ -256,9 +256,22 @@ def cpu_baseline(dist: str, n: int, seed: int, seconds: float, threads: int | No
         t0 = time.perf_counter()
         fill()
         times.append(time.perf_counter() - t0)
+    # one host thread, as SURVEY 8(d) asks beside the all-cores figure (the
+    # reference's numba fill runs ~0.25 G samples/s per thread in the build
+    # container): 2^26 samples into an array of its own, best of 3 after a warm-up
+    n1 = min(n, 1 << 26)
+    one = _CpuFill(dist, n1, seed, 1)
+    one()
+    t1 = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        one()
+        t1.append(time.perf_counter() - t0)
     return {"value": n / statistics.median(times), "best": n / min(times), "unit": UNIT,
             "cores": threads, "kind": "port", "reps": len(times),
-            "sample": _cpu_sample_desc(dist, n, threads, fill.full), "cpu_model": _cpu_model()}
+            "sample": _cpu_sample_desc(dist, n, threads, fill.full), "cpu_model": _cpu_model(),
+            "one_thread": {"value": n1 / min(t1), "unit": UNIT, "cores": 1,
+                           "sample": f"{dist} fp64, n={n1}, best of 3"}}
 
 
 def run_reference(args, rank: int):
